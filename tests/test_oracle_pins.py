@@ -1,0 +1,318 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names the passage / mathematical fact it checks.  A plausible mistake
+in the oracle (dropped term, wrong sign or index, transposed operand, wrong
+mirror, wrong weight) fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import integrate, signal
+
+from oracle import fbp_oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_worked_examples.json")))
+COEFF_DIR = os.path.join(os.path.dirname(os.path.dirname(__file__)), "coeffs")
+
+
+def load_coeffs(N=512, variant="dc0"):
+    c = json.load(open(os.path.join(COEFF_DIR, f"iir_q3_n{N}_{variant}.json")))
+    return np.array(c["b"]), np.array(c["a"]), c
+
+
+# ----------------------------------------------------------------- ramp kernel
+def test_ramp_kernel_spec_examples():
+    assert np.array_equal(O.ramp_kernel(0), np.array(GOLD["ramp_kernel_L0_0"]["taps"]))
+    g = GOLD["ramp_kernel_L0_2"]
+    assert np.allclose(O.ramp_kernel(2), g["taps"], atol=g["tol"])
+
+
+def test_ramp_kernel_equals_eq6_integral():
+    """Eq.6: h(n) = 2 int_0^{1/2} |w| e^{2 pi i w n} dw, by quadrature."""
+    h = O.ramp_kernel(9)
+    for n in range(-9, 10):
+        val, _ = integrate.quad(lambda w: 2.0 * w * math.cos(2 * math.pi * w * n), 0.0, 0.5,
+                                epsabs=1e-14, epsrel=1e-14, limit=200)
+        assert abs(val - h[n + 9]) < 1e-12, n
+
+
+def test_ramp_kernel_equals_eq6_sinc_form():
+    """Eq.6 right-hand side: sinc(pi n)/2 - sinc^2(pi n/2)/4 (numpy's normalised sinc)."""
+    n = np.arange(-50, 51)
+    rhs = np.sinc(n) / 2.0 - np.sinc(n / 2.0) ** 2 / 4.0
+    assert np.allclose(O.ramp_kernel(50), rhs, atol=1e-15)
+
+
+def test_ramp_kernel_dc_sum_closed_form():
+    """sum_n h(n) -> 0 (sum over odd k of 1/k^2 = pi^2/8); finite L0 leaves the tail."""
+    for L0 in (1, 7, 64, 1001):
+        s = O.ramp_kernel(L0).sum()
+        tail = 2.0 * sum(1.0 / (k * math.pi) ** 2 for k in range(L0 + 1 if L0 % 2 == 0 else L0 + 2, 200001, 2))
+        # remaining tail beyond 200001 < 2/(pi^2 * 200001) ~ 1e-6 / 1
+        assert abs(s - tail) < 2.0 / (math.pi ** 2 * 200000), L0
+
+
+def test_causal_target_split():
+    g = GOLD["causal_target_L0_2"]
+    assert np.allclose(O.causal_target(2), g["taps"], atol=g["tol"])
+    for L0 in (0, 5, 16):
+        hp = O.causal_target(L0)
+        h = O.ramp_kernel(L0)
+        full = np.concatenate([hp[::-1], [0.0] * 0])  # h-(n) = h+(-n)
+        rec = np.zeros(2 * L0 + 1)
+        rec[L0:] += hp
+        rec[: L0 + 1] += hp[::-1]
+        assert np.allclose(rec, h, atol=0), L0   # Eq.10/11 split exactness
+        assert len(full) == L0 + 1
+
+
+# ----------------------------------------------------------------------- IIR
+def test_iir_spec_examples():
+    g = GOLD["iir_geometric"]
+    r = O.iir_impulse_response(g["b"], g["a"], len(g["response"]) - 1)
+    assert np.array_equal(r, np.array(g["response"]))
+    g = GOLD["iir_pure_gain"]
+    r = O.iir_impulse_response(g["b"], g["a"], len(g["response"]) - 1)
+    assert np.array_equal(r, np.array(g["response"]))
+    # closed form 0.5^n over a long horizon
+    r = O.iir_impulse_response([1.0], [-0.5], 60)
+    assert np.array_equal(r, 0.5 ** np.arange(61))
+
+
+def test_iir_impulse_response_partial_fractions():
+    """Closed form from the roots of A(z): h(n) = sum_i r_i p_i^n (+ direct terms)."""
+    b, a, _ = load_coeffs(512, "spec")
+    n = np.arange(200)
+    r, p, k = signal.residuez(b, np.concatenate([[1.0], a]))
+    h = np.real(sum(ri * pi ** n for ri, pi in zip(r, p)))
+    for j, kj in enumerate(k):
+        h[j] += np.real(kj)
+    assert np.allclose(O.iir_impulse_response(b, a, 199), h, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant", ["spec", "dc0"])
+def test_iir_matches_lfilter(variant):
+    """Library routine: scipy.signal.lfilter forward, and on the reversed row."""
+    b, a, _ = load_coeffs(512, variant)
+    rng = np.random.default_rng(3)
+    x = rng.normal(size=(5, 300))
+    A = np.concatenate([[1.0], a])
+    yc = signal.lfilter(b, A, x, axis=-1)
+    ya = signal.lfilter(b, A, x[:, ::-1], axis=-1)[:, ::-1]
+    assert np.allclose(O.iir_causal(x, b, a), yc, atol=1e-12)
+    assert np.allclose(O.iir_anticausal(x, b, a), ya, atol=1e-12)
+    assert np.allclose(O.iir_symmetric(x, b, a), yc + ya, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant", ["spec", "dc0"])
+def test_iir_symmetric_equals_own_impulse_convolution(variant):
+    """North-star check 1: symmetric IIR == direct convolution with its
+    own two-sided impulse response g(m) = h(|m|), g(0) = 2 h(0) (Eq.10-12)."""
+    b, a, _ = load_coeffs(512, variant)
+    L = 256
+    h = O.iir_impulse_response(b, a, L)
+    g = np.concatenate([h[:0:-1], [2 * h[0]], h[1:]])       # lags -L..L
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(3, L))
+    ref = np.stack([np.convolve(row, g)[L: L + L] for row in x])
+    assert np.allclose(O.iir_symmetric(x, b, a), ref, atol=1e-9)
+
+
+def test_iir_symmetric_impulse_is_symmetric():
+    b, a, _ = load_coeffs(512, "spec")
+    x = np.zeros((1, 201))
+    x[0, 100] = 1.0
+    y = O.iir_symmetric(x, b, a)[0]
+    assert np.allclose(y[100 + np.arange(1, 100)], y[100 - np.arange(1, 100)], atol=1e-15)
+    assert abs(y[100] - 2 * b[0]) < 1e-15
+
+
+@pytest.mark.parametrize("variant", ["spec", "dc0"])
+def test_iir_fit_error_matches_frozen_file(variant):
+    """The frozen coefficients reproduce their recorded fit error against h+ (Eq.10)."""
+    b, a, c = load_coeffs(2048, variant)
+    K = c["K"]
+    e = O.iir_impulse_response(b, a, K) - O.causal_target(K)
+    assert abs(np.mean(e ** 2) - c["mse"]) <= 1e-6 * c["mse"]
+    assert np.all(np.abs(O.iir_poles(a)) < 1.0)
+    # the ramp approximation is good to the fit error: per-lag RMS ~ sqrt(mse)
+    assert math.sqrt(c["mse"]) < 1e-4
+
+
+def test_fir_filter_against_numpy_convolve():
+    taps = O.ramp_kernel(20)
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(2, 100))
+    ref = np.stack([np.convolve(r, taps)[20:120] for r in x])
+    assert np.allclose(O.fir_filter(x, taps), ref, atol=1e-13)
+
+
+# ------------------------------------------------------------- dyadic patterns
+def test_dyadic_table_N8_golden():
+    rows = GOLD["dyadic_offsets_N8"]["rows"]
+    ref = np.array([[int(c) for c in r] for r in rows])
+    assert np.array_equal(O.dyadic_offsets(8), ref)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8, 16, 32, 64, 128])
+def test_dyadic_properties(N):
+    d = O.dyadic_offsets(N)
+    assert np.array_equal(d, O.dyadic_offsets_closed_form(N))
+    assert np.array_equal(d, d.T)                       # d_t(y) = d_y(t)  (R5)
+    assert np.all(d[:, 0] == 0)
+    assert np.array_equal(d[:, N - 1], np.arange(N))     # pattern ends at shift t
+    if N > 1:
+        steps = np.diff(d, axis=1)
+        assert np.all((steps == 0) | (steps == 1))       # one pixel per row, connected
+        y = np.arange(N)
+        dev = np.abs(d - np.arange(N)[:, None] * y[None, :] / (N - 1))
+        assert dev.max() <= 0.5 + math.log2(N) / 4       # approximates a straight line
+
+
+# ---------------------------------------------------------- forward projection
+def test_forward_2x2_spec_example():
+    g = GOLD["fht_2x2"]
+    S = O.forward_project(np.array(g["image"], dtype=float))
+    assert list(S[0, 0, 2:4]) == g["Lv_plus_t0_cols_2_3"]
+    assert S[0, 1, 2] == g["Lv_plus_t1_col_2"]
+    g2 = GOLD["fht_2x2_all_families"]
+    assert np.array_equal(S, np.array(g2["S"], dtype=float))
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16])
+def test_forward_brute_force_and_fht_forward_bit_exact(N):
+    """FHT == brute-force dyadic sums on random integer images, exactly;
+    SPEC.md:44/475: every (family, t) row sums to the image total; t=0
+    rows of the v families are column sums."""
+    rng = np.random.default_rng(N)
+    for _ in range(3):
+        img = rng.integers(-50, 50, size=(N, N)).astype(float)
+        S = O.forward_project(img)
+        assert np.array_equal(S, O.fht_forward(img))
+        assert np.all(S.sum(axis=2) == img.sum())
+        assert np.array_equal(S[0, 0, N:], img.sum(axis=0))
+        assert np.array_equal(S[1, 0, N:], img.sum(axis=0)[::-1])
+        # support of row t is [N - t, 2N)   (R2)
+        for t in range(N):
+            assert np.all(S[:, t, : N - t] == 0)
+
+
+# ------------------------------------------------------------- back projection
+def test_backprojection_2x2_golden():
+    g = GOLD["fht_2x2_all_families"]
+    S = np.array(g["S"], dtype=float)
+    out = O.combine(O.fht_backproject(S), 1.0)
+    assert np.array_equal(out, np.array(g["unweighted_backprojection"], dtype=float))
+    assert np.array_equal(O.combine(O.backproject_direct(S), 1.0), out)
+
+
+def test_backprojection_impulse_peak():
+    g = GOLD["impulse_N4"]
+    img = np.zeros((4, 4))
+    img[g["y"], g["x"]] = 1.0
+    out = O.combine(O.fht_backproject(O.forward_project(img)), 1.0)
+    assert out[g["y"], g["x"]] == g["peak"] == out.max()
+    assert np.argmax(out) == g["y"] * 4 + g["x"]
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16])
+def test_backprojection_is_exact_adjoint(N):
+    """<R f, P> = <f, B P> exactly on integers: pins the back projection (incl. the
+    family un-mirror/un-transpose of Eq.20-22) to the pinned forward projection."""
+    rng = np.random.default_rng(100 + N)
+    img = rng.integers(-20, 20, size=(N, N)).astype(float)
+    P = rng.integers(-20, 20, size=(4, N, 2 * N)).astype(float)
+    lhs = float(np.sum(O.forward_project(img) * P))
+    rhs = float(np.sum(img * O.combine(O.backproject_direct(P), 1.0)))
+    assert lhs == rhs
+    rhs2 = float(np.sum(img * O.combine(O.fht_backproject(P), 1.0)))
+    assert lhs == rhs2
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64])
+def test_fht_backprojection_bit_exact_vs_direct_integers(N):
+    """North-star check 2: FHT == brute-force sums along every dyadic pattern, bit-exact."""
+    rng = np.random.default_rng(200 + N)
+    P = rng.integers(-511, 512, size=(4, N, 2 * N)).astype(float)
+    assert np.array_equal(O.fht_backproject(P), O.backproject_direct(P))
+    d = O.dyadic_offsets(N)
+    for _ in range(10):
+        f, y, x = rng.integers(0, 4), rng.integers(0, N), rng.integers(0, N)
+        assert O.backproject_pixel(P, f, y, x, d) == O.fht_backproject(P)[f, y, x]
+
+
+def test_fht_backprojection_float_vs_direct_N256():
+    """North-star check 3: direct Theta(N^3) BP == FHT BP to float64 rounding."""
+    N = 256
+    rng = np.random.default_rng(7)
+    P = rng.normal(size=(4, N, 2 * N))
+    A = O.fht_backproject(P)
+    B = O.backproject_direct(P)
+    assert np.max(np.abs(A - B)) <= 1e-12 * np.max(np.abs(B))
+
+
+def test_zero_in_zero_out():
+    b, a, _ = load_coeffs(64, "spec")
+    assert np.all(O.reconstruct(np.zeros((4, 8, 16)), b, a) == 0)
+
+
+# ------------------------------------------------- end-to-end convention pins
+def _raster_ellipses(N, ell):
+    """Point-sampled (pixel centres) ellipse phantom, test-local."""
+    yy, xx = np.mgrid[0:N, 0:N] + 0.5
+    img = np.zeros((N, N))
+    for cx, cy, a, b, phi, rho in ell:
+        u = (xx - cx) * math.cos(phi) + (yy - cy) * math.sin(phi)
+        v = -(xx - cx) * math.sin(phi) + (yy - cy) * math.cos(phi)
+        img += rho * ((u / a) ** 2 + (v / b) ** 2 <= 1.0)
+    return img
+
+
+def _phantom(N, seed):
+    rng = np.random.default_rng(seed)
+    ell = []
+    for _ in range(10):
+        r = 0.8 * N / 2 * math.sqrt(rng.uniform())
+        th = rng.uniform(0, 2 * math.pi)
+        ell.append((N / 2 + r * math.cos(th), N / 2 + r * math.sin(th),
+                    rng.uniform(N / 16, N / 4), rng.uniform(N / 16, N / 4),
+                    rng.uniform(0, math.pi), rng.uniform(0.2, 1.0)))
+    return _raster_ellipses(N, ell)
+
+
+def _fit(rec, ph):
+    scale = float(np.sum(rec * ph) / np.sum(ph * ph))
+    rel = float(np.sqrt(np.mean((rec - ph) ** 2)) / np.sqrt(np.mean(ph ** 2)))
+    return scale, rel
+
+
+@pytest.mark.parametrize("N", [32, 64])
+def test_fir_fbp_recovers_phantom_scale(N):
+    """Weight w = 1/N (R7) and the family geometry (R4): FIR-ramp-filtered (Eq.8,
+    L0 = 2N) FHT back projection of the dyadic projection of a phantom reproduces
+    it with best-fit scale 1 (a wrong weight, mirror or transpose gives 0.4-0.6 or 2)."""
+    ph = _phantom(N, 11)
+    S = O.fht_forward(ph)
+    F = O.fir_filter(S, O.ramp_kernel(2 * N))
+    rec = O.combine(O.fht_backproject(F), 1.0 / N)
+    scale, rel = _fit(rec, ph)
+    assert abs(scale - 1.0) < 0.03, scale
+    assert rel < 0.12, rel
+
+
+def test_iir_fbp_dc0_recovers_phantom():
+    """Quality sanity (not parity): the fitted M=Q=3 zero-DC recursive pair (Eq.12-13)
+    gives a recognisable reconstruction at N=64 (scale 0.84, rel-RMSE 0.24 measured).
+    The 3-pole fit cannot follow the 1/n^2 tail of Eq.7, so quality falls with N
+    (DESIGN.md §3 R14); coefficients are an input, parity does not depend on them."""
+    N = 64
+    b, a, _ = load_coeffs(N, "dc0")
+    ph = _phantom(N, 12)
+    S = O.fht_forward(ph)
+    rec = O.reconstruct(S, b, a)
+    scale, rel = _fit(rec, ph)
+    assert abs(scale - 1.0) < 0.25, scale
+    assert rel < 0.35, rel
