@@ -33,7 +33,7 @@ import numpy as np
 __all__ = [
     "ramp_kernel", "causal_target", "iir_impulse_response", "iir_causal",
     "iir_anticausal", "iir_symmetric", "fir_filter", "dyadic_offsets",
-    "dyadic_offsets_closed_form", "family_views", "forward_project",
+    "dyadic_offsets_closed_form", "dyadic_offsets_column", "family_views", "forward_project",
     "backproject_direct", "backproject_pixel", "fht_backproject", "combine",
     "reconstruct", "iir_poles", "fht_forward",
 ]
@@ -257,18 +257,29 @@ def forward_project(img: np.ndarray) -> np.ndarray:
     return S
 
 
+def dyadic_offsets_column(N: int, y: int) -> np.ndarray:
+    """d_t(y) for all t at one row y, by the closed form of R3 (vectorised over t)."""
+    n = N.bit_length() - 1
+    t = np.arange(N, dtype=np.int64)
+    v = np.zeros(N, dtype=np.int64)
+    for k in range(n):
+        if (y >> (n - 1 - k)) & 1:
+            v += ((t >> k) + 1) // 2
+    return v
+
+
 def backproject_pixel(F: np.ndarray, f: int, y: int, x: int, d=None) -> float:
     """One pixel of the family-f back projection, direct definition (O5).
 
     PAPER.md:204-212 (Eq.18-19) read as the exact adjoint of ``forward_project``
-    (R4, R5): B_f[y][x] = sum_{t=0}^{N-1} F[f][t][x + N - d_t(y)].
+    (R4, R5): B_f[y][x] = sum_{t=0}^{N-1} F[f][t][x + N - d_t(y)], summed in
+    order t = 0..N-1.  ``d`` is an optional full table d[t][y].
     """
     N = F.shape[1]
-    if d is None:
-        d = dyadic_offsets(N)
+    col = dyadic_offsets_column(N, y) if d is None else np.asarray(d)[:, y]
     acc = 0.0
     for t in range(N):
-        acc += float(F[f, t, x + N - d[t, y]])
+        acc += float(F[f, t, x + N - col[t]])
     return acc
 
 

@@ -1,0 +1,527 @@
+// C-ABI layer of libfbp (include/fbp.h): validation, plan (coefficient tables,
+// level split, workspace), and stream-ordered orchestration of the kernels.
+#include "../../include/fbp.h"
+#include "fbp_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace fbp;
+
+struct fbp_plan {
+  Geometry g;
+  IirParams iir;
+  int device = 0;
+  int max_batch = 1;
+  int group = 1;            // slices per workspace group
+  float* F = nullptr;       // filtered linogram workspace [group][4][N][2N]
+  float* R = nullptr;       // pass-A output workspace [group][4][NB][H][WR]
+  size_t F_bytes = 0, R_bytes = 0;
+  // host-path staging (allocated lazily by fbp_reconstruct_host)
+  float* d_in[2] = {nullptr, nullptr};
+  float* d_out[2] = {nullptr, nullptr};
+  float* h_in[2] = {nullptr, nullptr};
+  float* h_out[2] = {nullptr, nullptr};
+  cudaStream_t s_copy = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  mutable long long launches = 0;
+  // per-kernel event timing (fbp_plan_profile)
+  mutable bool profiling = false;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  mutable std::vector<Rec> recs;
+  mutable std::vector<cudaEvent_t> pool;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fbp_status fail(fbp_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+fbp_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(FBP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Schur-Cohn / step-down test: all roots of z^Q + a1 z^{Q-1} + ... + aQ strictly
+// inside the unit circle iff every reflection coefficient has |k| < 1.
+bool stable(int q, const double* a) {
+  std::vector<double> c(a, a + q);
+  for (int ord = q; ord >= 1; --ord) {
+    const double k = c[ord - 1];
+    if (!(std::fabs(k) < 1.0)) return false;
+    const double den = 1.0 - k * k;
+    std::vector<double> nc(ord - 1);
+    for (int i = 1; i <= ord - 1; ++i) nc[i - 1] = (c[i - 1] - k * c[ord - i - 1]) / den;
+    c.swap(nc);
+  }
+  return true;
+}
+
+// Companion matrix of A(z) acting on the state (y[n], y[n-1], ..., y[n-QM+1]).
+void companion(int QM, const double* a_pad, std::vector<double>& A) {
+  A.assign((size_t)QM * QM, 0.0);
+  for (int j = 0; j < QM; ++j) A[j] = -a_pad[j];
+  for (int i = 1; i < QM; ++i) A[(size_t)i * QM + (i - 1)] = 1.0;
+}
+
+void matmul(int n, const std::vector<double>& X, const std::vector<double>& Y,
+            std::vector<double>& Z) {
+  std::vector<double> T((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k)
+      for (int j = 0; j < n; ++j) T[(size_t)i * n + j] += X[(size_t)i * n + k] * Y[(size_t)k * n + j];
+  Z.swap(T);
+}
+
+void matpow(int n, const std::vector<double>& X, long long e, std::vector<double>& Z) {
+  std::vector<double> R((size_t)n * n, 0.0), B = X;
+  for (int i = 0; i < n; ++i) R[(size_t)i * n + i] = 1.0;
+  while (e > 0) {
+    if (e & 1) matmul(n, R, B, R);
+    matmul(n, B, B, B);
+    e >>= 1;
+  }
+  Z.swap(R);
+}
+
+Geometry make_geometry(int N, int qm) {
+  Geometry g{};
+  int n = 0;
+  while ((1 << n) < N) ++n;
+  g.n = n;
+  g.N = N;
+  g.W = 2 * N;
+  g.k1 = (n + 1) / 2;
+  g.m = n - g.k1;
+  g.H = 1 << g.k1;
+  g.NB = 1 << g.m;
+  g.WR = N + g.NB;
+  g.XA = std::min(128, g.W);
+  while (g.XA > 16 && (size_t)2 * g.H * (g.XA + g.H - 1) * 4 > 200 * 1024) g.XA /= 2;
+  g.XB = std::min(128, N);
+  while (g.XB > 16 && (size_t)4 * g.NB * (g.XB + g.NB - 1) * 4 > 200 * 1024) g.XB /= 2;
+  g.L = (g.W >= 32) ? g.W / 32 : 1;
+  g.iir_qm = qm;
+  return g;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+fbp_status check_call(const fbp_plan* plan, const void* in, const void* out, int batch) {
+  if (!plan) return fail(FBP_ERR_PARAM, "plan is NULL");
+  if (batch < 0 || batch > plan->max_batch)
+    return fail(FBP_ERR_PARAM, "batch " + std::to_string(batch) + " outside [0, max_batch=" +
+                                   std::to_string(plan->max_batch) + "]");
+  if (batch == 0) return FBP_OK;
+  if (!in || !out) return fail(FBP_ERR_PARAM, "NULL data pointer");
+  if (!aligned16(in) || !aligned16(out)) return fail(FBP_ERR_PARAM, "pointer not 16-byte aligned");
+  return FBP_OK;
+}
+
+cudaEvent_t pool_get(const fbp_plan* p) {
+  if (!p->pool.empty()) {
+    cudaEvent_t e = p->pool.back();
+    p->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Run one kernel launcher; when profiling, bracket it with events on its stream.
+template <typename Fn>
+cudaError_t timed(const fbp_plan* p, int kind, cudaStream_t st, Fn&& fn) {
+  if (!p->profiling) return fn();
+  cudaEvent_t a = pool_get(p), b = pool_get(p);
+  cudaEventRecord(a, st);
+  cudaError_t e = fn();
+  cudaEventRecord(b, st);
+  p->recs.push_back({kind, a, b});
+  return e;
+}
+
+// FHT back projection of `slices` linograms (device) into images, via plan->R.
+cudaError_t run_backproject(const fbp_plan* p, const float* lin, float* img, int slices,
+                            float scale, cudaStream_t st, int* launches) {
+  cudaError_t e = timed(p, 1, st, [&] { return launch_fht_pass_a(lin, p->R, slices, p->g, st, launches); });
+  if (e != cudaSuccess) return e;
+  e = timed(p, 2, st, [&] { return launch_fht_pass_b(p->R, img, slices, 0, scale, p->g, st, launches); });
+  if (e != cudaSuccess) return e;
+  return timed(p, 2, st, [&] { return launch_fht_pass_b(p->R, img, slices, 1, scale, p->g, st, launches); });
+}
+
+cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, int batch,
+                            cudaStream_t st, int* launches) {
+  const Geometry& g = p->g;
+  const long long lin_elems = 4LL * g.N * g.W;
+  const long long img_elems = (long long)g.N * g.N;
+  const float w = 1.0f / (float)g.N;  // exact power of two (R7)
+  for (int s0 = 0; s0 < batch; s0 += p->group) {
+    const int ns = std::min(p->group, batch - s0);
+    cudaError_t e = timed(p, 0, st, [&] {
+      return launch_iir_rows(sino + s0 * lin_elems, p->F, (long long)ns * 4 * g.N, g, p->iir, st,
+                             launches);
+    });
+    if (e != cudaSuccess) return e;
+    e = run_backproject(p, p->F, img + s0 * img_elems, ns, w, st, launches);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fbp_status_str(fbp_status s) {
+  switch (s) {
+    case FBP_OK: return "FBP_OK";
+    case FBP_ERR_PLAN: return "FBP_ERR_PLAN: N must be a power of two in [2, 8192]";
+    case FBP_ERR_PARAM: return "FBP_ERR_PARAM: invalid argument";
+    case FBP_ERR_UNSTABLE: return "FBP_ERR_UNSTABLE: feedback polynomial has a root with |z| >= 1";
+    case FBP_ERR_CUDA: return "FBP_ERR_CUDA: CUDA runtime error";
+    case FBP_ERR_NOMEM: return "FBP_ERR_NOMEM: workspace allocation failed";
+    case FBP_ERR_DEVICE: return "FBP_ERR_DEVICE: device missing or not sm_100";
+  }
+  return "unknown fbp_status";
+}
+
+const char* fbp_last_error(void) { return g_last_error.c_str(); }
+
+fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const double* b, int q,
+                           const double* a, int device) {
+  g_last_error.clear();
+  if (!out) return fail(FBP_ERR_PARAM, "out is NULL");
+  *out = nullptr;
+  if (n < 2 || n > 8192 || (n & (n - 1)) != 0)
+    return fail(FBP_ERR_PLAN, "N=" + std::to_string(n) + " is not a power of two in [2, 8192]");
+  if (max_batch < 1) return fail(FBP_ERR_PARAM, "max_batch must be >= 1");
+  if (m < 1 || m > kMaxOrder || q < 0 || q > kMaxOrder)
+    return fail(FBP_ERR_PARAM, "orders must satisfy 1 <= M <= 8, 0 <= Q <= 8");
+  if (!b || (q > 0 && !a)) return fail(FBP_ERR_PARAM, "NULL coefficient pointer");
+  for (int i = 0; i < m; ++i)
+    if (!std::isfinite(b[i])) return fail(FBP_ERR_PARAM, "non-finite b coefficient");
+  for (int i = 0; i < q; ++i)
+    if (!std::isfinite(a[i])) return fail(FBP_ERR_PARAM, "non-finite a coefficient");
+  if (!stable(q, a)) return fail(FBP_ERR_UNSTABLE, "feedback polynomial is not stable");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return fail(FBP_ERR_DEVICE, "CUDA device " + std::to_string(device) + " not available");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+    return fail(FBP_ERR_DEVICE, "cudaGetDeviceProperties failed");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FBP_ERR_DEVICE, std::string("device is sm_") + std::to_string(prop.major) +
+                                    std::to_string(prop.minor) + ", libfbp is built for sm_100a");
+  DeviceGuard guard(device);
+
+  fbp_plan* p = new fbp_plan();
+  p->device = device;
+  p->max_batch = max_batch;
+  const int qm = (std::max(m - 1, q) <= 3) ? 3 : 8;
+  p->g = make_geometry(n, qm);
+
+  // ---- coefficient tables (double on the host, fp32 for the kernels) ----
+  double beta = 0.0;
+  for (int i = 0; i < m; ++i) beta += b[i];
+  std::memset(&p->iir, 0, sizeof(p->iir));
+  p->iir.beta = (float)beta;
+  for (int k = 0; k < m - 1; ++k) {
+    double s = 0.0;
+    for (int j = k + 1; j < m; ++j) s += b[j];
+    p->iir.c[k] = (float)(-s);
+  }
+  std::vector<double> apad(qm, 0.0);
+  for (int k = 0; k < q; ++k) {
+    apad[k] = a[k];
+    p->iir.a[k] = (float)a[k];
+  }
+  std::vector<double> A, Pk;
+  companion(qm, apad.data(), A);
+  for (int k = 0; k < kScanSteps; ++k) {
+    matpow(qm, A, (long long)p->g.L << k, Pk);
+    for (int i = 0; i < qm; ++i)
+      for (int j = 0; j < qm; ++j) p->iir.P[k][i * kMaxOrder + j] = (float)Pk[(size_t)i * qm + j];
+  }
+
+  // ---- workspace, sized for a group of slices ----
+  const Geometry& g = p->g;
+  const size_t f_slice = (size_t)4 * g.N * g.W * sizeof(float);
+  const size_t r_slice = (size_t)4 * g.NB * g.H * g.WR * sizeof(float);
+  const size_t budget = (size_t)256 << 20;
+  long long grp = (long long)(budget / (f_slice + r_slice));
+  grp = std::max<long long>(1, std::min<long long>(grp, max_batch));
+  grp = std::min<long long>(grp, 16383);
+  p->group = (int)grp;
+  p->F_bytes = f_slice * p->group;
+  p->R_bytes = r_slice * p->group;
+  if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    fbp_plan_destroy(p);
+    return fail(FBP_ERR_NOMEM, "workspace allocation failed");
+  }
+  // Entries of R that pass A never writes are read (and discarded) by pass B.
+  cudaError_t e = cudaMemset(p->R, 0, p->R_bytes);
+  if (e != cudaSuccess) {
+    fbp_plan_destroy(p);
+    return cuda_fail(e, "cudaMemset");
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fbp_plan_destroy(p);
+    return cuda_fail(e, "plan init");
+  }
+  *out = p;
+  return FBP_OK;
+}
+
+void fbp_plan_destroy(fbp_plan* p) {
+  if (!p) return;
+  DeviceGuard guard(p->device);
+  cudaFree(p->F);
+  cudaFree(p->R);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(p->d_in[i]);
+    cudaFree(p->d_out[i]);
+    cudaFreeHost(p->h_in[i]);
+    cudaFreeHost(p->h_out[i]);
+  }
+  if (p->s_copy) cudaStreamDestroy(p->s_copy);
+  if (p->s_comp) cudaStreamDestroy(p->s_comp);
+  if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+  for (auto& r : p->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : p->pool) cudaEventDestroy(e);
+  delete p;
+}
+
+fbp_status fbp_iir_filter(const fbp_plan* p, const float* sino, float* filtered, int batch,
+                          void* stream) {
+  fbp_status s = check_call(p, sino, filtered, batch);
+  if (s != FBP_OK || batch == 0) return s;
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  cudaError_t e = timed(p, 0, (cudaStream_t)stream, [&] {
+    return launch_iir_rows(sino, filtered, (long long)batch * 4 * p->g.N, p->g, p->iir,
+                           (cudaStream_t)stream, &launches);
+  });
+  p->launches = launches;
+  if (e != cudaSuccess) return cuda_fail(e, "fbp_iir_filter");
+  return FBP_OK;
+}
+
+fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image, int batch,
+                               float scale, void* stream) {
+  fbp_status s = check_call(p, lin, image, batch);
+  if (s != FBP_OK || batch == 0) return s;
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  const long long lin_elems = 4LL * p->g.N * p->g.W;
+  const long long img_elems = (long long)p->g.N * p->g.N;
+  for (int s0 = 0; s0 < batch; s0 += p->group) {
+    const int ns = std::min(p->group, batch - s0);
+    cudaError_t e = run_backproject(p, lin + s0 * lin_elems, image + s0 * img_elems, ns, scale,
+                                    (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) {
+      p->launches = launches;
+      return cuda_fail(e, "fbp_fht_backproject");
+    }
+  }
+  p->launches = launches;
+  return FBP_OK;
+}
+
+fbp_status fbp_reconstruct(const fbp_plan* p, const float* sino, float* image, int batch,
+                           void* stream) {
+  fbp_status s = check_call(p, sino, image, batch);
+  if (s != FBP_OK || batch == 0) return s;
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  cudaError_t e = run_reconstruct(p, sino, image, batch, (cudaStream_t)stream, &launches);
+  p->launches = launches;
+  if (e != cudaSuccess) return cuda_fail(e, "fbp_reconstruct");
+  return FBP_OK;
+}
+
+fbp_status fbp_reconstruct_host(const fbp_plan* cp, const float* sino, float* image, int batch) {
+  if (!cp) return fail(FBP_ERR_PARAM, "plan is NULL");
+  if (batch < 0) return fail(FBP_ERR_PARAM, "batch < 0");
+  if (batch == 0) return FBP_OK;
+  if (!sino || !image) return fail(FBP_ERR_PARAM, "NULL data pointer");
+  fbp_plan* p = const_cast<fbp_plan*>(cp);
+  DeviceGuard guard(p->device);
+  const Geometry& g = p->g;
+  const size_t lin_elems = (size_t)4 * g.N * g.W;
+  const size_t img_elems = (size_t)g.N * g.N;
+  const int grp = p->group;
+  cudaError_t e;
+  // Are the caller's buffers page-locked?  Then copy directly, else stage.
+  auto pinned = [](const void* ptr) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool in_pinned = pinned(sino), out_pinned = pinned(image);
+  if (!p->s_copy) {
+    if ((e = cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream create");
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (!p->d_in[i]) {
+      if (cudaMalloc(&p->d_in[i], lin_elems * grp * 4) != cudaSuccess ||
+          cudaMalloc(&p->d_out[i], img_elems * grp * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FBP_ERR_NOMEM, "host-path device buffers");
+      }
+    }
+    if (!in_pinned && !p->h_in[i] && cudaMallocHost(&p->h_in[i], lin_elems * grp * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FBP_ERR_NOMEM, "pinned staging");
+    }
+    if (!out_pinned && !p->h_out[i] && cudaMallocHost(&p->h_out[i], img_elems * grp * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FBP_ERR_NOMEM, "pinned staging");
+    }
+  }
+  cudaEvent_t ev_in[2], ev_done[2], ev_out[2];
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming);
+    cudaEventRecord(ev_out[i], p->s_d2h);
+  }
+  int launches = 0;
+  const int ngroups = (batch + grp - 1) / grp;
+  // pending D2H (unpinned output) bookkeeping
+  std::vector<int> out_group(2, -1);
+  auto flush_out = [&](int slot) {
+    if (out_group[slot] < 0) return;
+    cudaEventSynchronize(ev_out[slot]);
+    const int g0 = out_group[slot] * grp;
+    const int ns = std::min(grp, batch - g0);
+    std::memcpy(image + (size_t)g0 * img_elems, p->h_out[slot], (size_t)ns * img_elems * 4);
+    out_group[slot] = -1;
+  };
+  e = cudaSuccess;
+  for (int gi = 0; gi < ngroups && e == cudaSuccess; ++gi) {
+    const int slot = gi & 1;
+    const int s0 = gi * grp;
+    const int ns = std::min(grp, batch - s0);
+    const size_t in_bytes = (size_t)ns * lin_elems * 4, out_bytes = (size_t)ns * img_elems * 4;
+    // slot reuse: previous compute on this slot must be done before overwriting d_in
+    cudaStreamWaitEvent(p->s_copy, ev_done[slot], 0);
+    const float* src = sino + (size_t)s0 * lin_elems;
+    if (!in_pinned) {
+      cudaEventSynchronize(ev_in[slot]);  // staging buffer free
+      std::memcpy(p->h_in[slot], src, in_bytes);
+      src = p->h_in[slot];
+    }
+    if ((e = cudaMemcpyAsync(p->d_in[slot], src, in_bytes, cudaMemcpyHostToDevice, p->s_copy)) != cudaSuccess) break;
+    cudaEventRecord(ev_in[slot], p->s_copy);
+    cudaStreamWaitEvent(p->s_comp, ev_in[slot], 0);
+    cudaStreamWaitEvent(p->s_comp, ev_out[slot], 0);  // d_out[slot] drained
+    if ((e = run_reconstruct(p, p->d_in[slot], p->d_out[slot], ns, p->s_comp, &launches)) != cudaSuccess) break;
+    cudaEventRecord(ev_done[slot], p->s_comp);
+    cudaStreamWaitEvent(p->s_d2h, ev_done[slot], 0);
+    flush_out(slot);
+    float* dst = out_pinned ? image + (size_t)s0 * img_elems : p->h_out[slot];
+    if ((e = cudaMemcpyAsync(dst, p->d_out[slot], out_bytes, cudaMemcpyDeviceToHost, p->s_d2h)) != cudaSuccess) break;
+    cudaEventRecord(ev_out[slot], p->s_d2h);
+    if (!out_pinned) out_group[slot] = gi;
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_copy);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_comp);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_d2h);
+  for (int i = 0; i < 2; ++i) flush_out(i);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_done[i]);
+    cudaEventDestroy(ev_out[i]);
+  }
+  p->launches = launches;
+  if (e != cudaSuccess) return cuda_fail(e, "fbp_reconstruct_host");
+  return FBP_OK;
+}
+
+long long fbp_plan_launch_count(const fbp_plan* p) { return p ? p->launches : -1; }
+
+fbp_status fbp_plan_profile(fbp_plan* p, int enable) {
+  if (!p) return fail(FBP_ERR_PARAM, "plan is NULL");
+  DeviceGuard guard(p->device);
+  for (auto& r : p->recs) {
+    cudaEventSynchronize(r.b);
+    p->pool.push_back(r.a);
+    p->pool.push_back(r.b);
+  }
+  p->recs.clear();
+  p->profiling = enable != 0;
+  return FBP_OK;
+}
+
+fbp_status fbp_plan_kernel_times(fbp_plan* p, double* ms, long long* launches, int kinds) {
+  if (!p || kinds < 0 || kinds > 3 || (kinds > 0 && (!ms || !launches)))
+    return fail(FBP_ERR_PARAM, "fbp_plan_kernel_times: bad arguments");
+  DeviceGuard guard(p->device);
+  for (int k = 0; k < kinds; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  cudaError_t err = cudaSuccess;
+  for (auto& r : p->recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) err = e;
+    if (r.kind < kinds) {
+      ms[r.kind] += t;
+      launches[r.kind] += 1;
+    }
+    p->pool.push_back(r.a);
+    p->pool.push_back(r.b);
+  }
+  p->recs.clear();
+  if (err != cudaSuccess) return cuda_fail(err, "fbp_plan_kernel_times");
+  return FBP_OK;
+}
+
+fbp_status fbp_plan_info(const fbp_plan* p, int* n, int* k1, int* m, int* group,
+                         long long* workspace_bytes) {
+  if (!p) return fail(FBP_ERR_PARAM, "plan is NULL");
+  if (n) *n = p->g.N;
+  if (k1) *k1 = p->g.k1;
+  if (m) *m = p->g.m;
+  if (group) *group = p->group;
+  if (workspace_bytes) *workspace_bytes = (long long)(p->F_bytes + p->R_bytes);
+  return FBP_OK;
+}
+
+}  // extern "C"

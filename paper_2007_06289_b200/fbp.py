@@ -1,0 +1,201 @@
+"""Thin ctypes binding of libfbp (include/fbp.h).  Argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this
+module never computes anything itself and has no CPU fallback: if libfbp.so is
+missing or the device is not an sm_100 B200 it raises.
+
+    plan = Plan(n=2048, b=[...], a=[...], max_batch=64, device=0)
+    img  = plan.reconstruct(sino)            # sino: float32 cuda [B, 4, N, 2N]
+    F    = plan.iir_filter(sino)             # Eq.12-13
+    bp   = plan.backproject(F, scale=1/N)    # Eq.19-22
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfbp.so")
+_lib = None
+
+FBP_STATUS = {0: "FBP_OK", 1: "FBP_ERR_PLAN", 2: "FBP_ERR_PARAM", 3: "FBP_ERR_UNSTABLE",
+              4: "FBP_ERR_CUDA", 5: "FBP_ERR_NOMEM", 6: "FBP_ERR_DEVICE"}
+
+EXPORTED = ["fbp_plan_create", "fbp_plan_destroy", "fbp_iir_filter", "fbp_fht_backproject",
+            "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
+            "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_profile", "fbp_plan_kernel_times"]
+
+KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b")
+
+
+class FbpError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{FBP_STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+def lib():
+    """Load libfbp.so (built in-tree by paper_2007_06289_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built: run `python -m paper_2007_06289_b200.build`")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, i, f, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.POINTER(ctypes.c_double)
+    L.fbp_plan_create.argtypes = [ctypes.POINTER(vp), i, i, i, d, i, d, i]
+    L.fbp_plan_create.restype = i
+    L.fbp_plan_destroy.argtypes = [vp]
+    L.fbp_plan_destroy.restype = None
+    L.fbp_iir_filter.argtypes = [vp, vp, vp, i, vp]
+    L.fbp_iir_filter.restype = i
+    L.fbp_fht_backproject.argtypes = [vp, vp, vp, i, f, vp]
+    L.fbp_fht_backproject.restype = i
+    L.fbp_reconstruct.argtypes = [vp, vp, vp, i, vp]
+    L.fbp_reconstruct.restype = i
+    L.fbp_reconstruct_host.argtypes = [vp, vp, vp, i]
+    L.fbp_reconstruct_host.restype = i
+    L.fbp_status_str.argtypes = [i]
+    L.fbp_status_str.restype = ctypes.c_char_p
+    L.fbp_last_error.argtypes = []
+    L.fbp_last_error.restype = ctypes.c_char_p
+    L.fbp_plan_launch_count.argtypes = [vp]
+    L.fbp_plan_launch_count.restype = ctypes.c_longlong
+    L.fbp_plan_info.argtypes = [vp] + [ctypes.POINTER(i)] * 4 + [ctypes.POINTER(ctypes.c_longlong)]
+    L.fbp_plan_info.restype = i
+    L.fbp_plan_profile.argtypes = [vp, i]
+    L.fbp_plan_profile.restype = i
+    L.fbp_plan_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_longlong), i]
+    L.fbp_plan_kernel_times.restype = i
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise FbpError(status, lib().fbp_last_error().decode())
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Plan:
+    """fbp_plan: N, IIR coefficients (Eq.9 sign), workspace on one device."""
+
+    def __init__(self, n: int, b, a, max_batch: int = 1, device: int = 0):
+        L = lib()
+        self.n = int(n)
+        self.b = [float(v) for v in b]
+        self.a = [float(v) for v in a]
+        self.max_batch = int(max_batch)
+        self.device = int(device)
+        bb = (ctypes.c_double * max(1, len(self.b)))(*self.b)
+        aa = (ctypes.c_double * max(1, len(self.a)))(*self.a)
+        h = ctypes.c_void_p()
+        _check(L.fbp_plan_create(ctypes.byref(h), self.n, self.max_batch, len(self.b), bb,
+                                 len(self.a), aa, self.device))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fbp_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- info
+    def info(self) -> dict:
+        n, k1, m, grp = (ctypes.c_int() for _ in range(4))
+        ws = ctypes.c_longlong()
+        _check(lib().fbp_plan_info(self._h, ctypes.byref(n), ctypes.byref(k1), ctypes.byref(m),
+                                   ctypes.byref(grp), ctypes.byref(ws)))
+        return dict(N=n.value, k1=k1.value, m=m.value, group=grp.value, workspace_bytes=ws.value)
+
+    def launch_count(self) -> int:
+        """Kernels launched by the last call on this plan."""
+        return int(lib().fbp_plan_launch_count(self._h))
+
+    def profile(self, enable: bool = True):
+        """Enable (and clear) / disable per-kernel CUDA-event timing inside libfbp."""
+        _check(lib().fbp_plan_profile(self._h, int(bool(enable))))
+
+    def kernel_times(self) -> dict:
+        """{kind: (total_ms, launches)} since the last profile(True); clears the record."""
+        ms = (ctypes.c_double * 3)()
+        n = (ctypes.c_longlong * 3)()
+        _check(lib().fbp_plan_kernel_times(self._h, ms, n, 3))
+        return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_KINDS)}
+
+    # ------------------------------------------------------------- checks
+    def _lin(self, x: torch.Tensor, name: str) -> torch.Tensor:
+        N = self.n
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32):
+            raise TypeError(f"{name} must be a float32 CUDA tensor")
+        if x.dim() == 3:
+            x = x.unsqueeze(0)
+        if tuple(x.shape[1:]) != (4, N, 2 * N):
+            raise ValueError(f"{name} must have shape [B, 4, {N}, {2 * N}], got {tuple(x.shape)}")
+        if not x.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        return x
+
+    def _img_out(self, out, B):
+        N = self.n
+        if out is None:
+            return torch.empty((B, N, N), device=f"cuda:{self.device}", dtype=torch.float32)
+        if tuple(out.shape) != (B, N, N) or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float32 [B, N, N] tensor")
+        return out
+
+    # ---------------------------------------------------------------- ops
+    def iir_filter(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        x = self._lin(sino, "sino")
+        out = torch.empty_like(x) if out is None else self._lin(out, "out")
+        _check(lib().fbp_iir_filter(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
+                                    _stream_ptr(stream)))
+        return out
+
+    def backproject(self, lin: torch.Tensor, scale: float = 1.0, out: torch.Tensor | None = None,
+                    stream=None):
+        x = self._lin(lin, "lin")
+        out = self._img_out(out, x.shape[0])
+        _check(lib().fbp_fht_backproject(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
+                                         float(scale), _stream_ptr(stream)))
+        return out
+
+    def reconstruct(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        x = self._lin(sino, "sino")
+        out = self._img_out(out, x.shape[0])
+        _check(lib().fbp_reconstruct(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
+                                     _stream_ptr(stream)))
+        return out
+
+    def reconstruct_host(self, sino, out=None):
+        """Host buffers in, host buffers out (numpy or CPU torch, float32, contiguous)."""
+        N = self.n
+        if isinstance(sino, torch.Tensor):
+            if sino.is_cuda or sino.dtype != torch.float32 or not sino.is_contiguous():
+                raise TypeError("sino must be a contiguous float32 CPU tensor")
+            B = sino.shape[0]
+            if out is None:
+                out = torch.empty((B, N, N), dtype=torch.float32, pin_memory=sino.is_pinned())
+            ptr_in, ptr_out = sino.data_ptr(), out.data_ptr()
+        else:
+            sino = np.ascontiguousarray(sino, dtype=np.float32)
+            B = sino.shape[0]
+            if out is None:
+                out = np.empty((B, N, N), dtype=np.float32)
+            ptr_in, ptr_out = sino.ctypes.data, out.ctypes.data
+        if tuple(sino.shape[1:]) != (4, N, 2 * N):
+            raise ValueError("sino must have shape [B, 4, N, 2N]")
+        _check(lib().fbp_reconstruct_host(self._h, ptr_in, ptr_out, B))
+        return out

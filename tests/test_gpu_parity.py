@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle (-m gpu).
+
+Tolerances (north_star):
+  * FHT back projection on integer-valued input: bit-exact.
+  * fp32 reconstruction / filtering: max |gpu - oracle| <= 1e-4 * max |oracle|
+    per slice.
+The oracle sees exactly the fp32 bytes the GPU sees (converted to float64).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import phantoms as P
+from oracle import fbp_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = 1e-4
+
+
+def coeffs(N, variant="dc0"):
+    c = json.load(open(os.path.join(ROOT, "coeffs", f"iir_q3_n{min(max(N, 64), 4096)}_{variant}.json")))
+    return c["b"], c["a"]
+
+
+@pytest.fixture(scope="module")
+def fbp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2007_06289_b200 import build
+    build.build()
+    import paper_2007_06289_b200 as pkg
+    return pkg
+
+
+def rel_err(gpu, ref):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(gpu - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+# -------------------------------------------------------------------- FHT BP
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64, 128, 256, 512])
+def test_backproject_integer_bit_exact(fbp, N):
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=3)
+    lin = P.integer_linogram(N, 3, seed=N)
+    out = plan.backproject(lin.cuda(), scale=1.0).cpu().numpy()
+    for i in range(3):
+        ref = O.combine(O.fht_backproject(lin[i].numpy().astype(np.float64)), 1.0)
+        assert np.array_equal(out[i].astype(np.float64), ref), (N, i)
+    # power-of-two weight stays exact
+    out2 = plan.backproject(lin.cuda(), scale=1.0 / N).cpu().numpy()
+    ref = O.combine(O.fht_backproject(lin[2].numpy().astype(np.float64)), 1.0 / N)
+    assert np.array_equal(out2[2].astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("N", [1024, 2048, 4096])
+def test_backproject_integer_bit_exact_sampled_full_size(fbp, N):
+    """Full sizes: sampled pixels, each summed by the oracle along its dyadic lines."""
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    lin = P.integer_linogram(N, 1, seed=7 + N)
+    out = plan.backproject(lin.cuda(), scale=1.0).cpu().numpy()[0]
+    L = lin[0].numpy().astype(np.float64)
+    d = None
+    rng = np.random.default_rng(N)
+    pts = [(0, 0), (N - 1, N - 1), (0, N - 1), (N - 1, 0)] + [tuple(rng.integers(0, N, 2)) for _ in range(12)]
+    for (y, x) in pts:
+        ref = (O.backproject_pixel(L, 0, y, x, d) + O.backproject_pixel(L, 1, y, N - 1 - x, d)
+               + O.backproject_pixel(L, 2, x, y, d) + O.backproject_pixel(L, 3, x, N - 1 - y, d))
+        assert float(out[y, x]) == ref, (N, y, x)
+
+
+def test_backproject_float_random(fbp):
+    N = 256
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    lin = P.random_linogram(N, 2, seed=3, scale=10.0)
+    out = plan.backproject(lin.cuda(), scale=1.0 / N).cpu().numpy()
+    for i in range(2):
+        ref = O.combine(O.fht_backproject(lin[i].double().numpy()), 1.0 / N)
+        assert rel_err(out[i], ref) < 1e-6
+
+
+# ----------------------------------------------------------------------- IIR
+@pytest.mark.parametrize("N,variant", [(2, "dc0"), (4, "spec"), (8, "dc0"), (16, "dc0"), (64, "spec"),
+                                       (64, "dc0"), (512, "dc0"), (2048, "spec")])
+def test_iir_filter_random(fbp, N, variant):
+    b, a = coeffs(N, variant)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    x = P.random_linogram(N, 2 if N <= 512 else 1, seed=11 + N, scale=100.0)
+    y = plan.iir_filter(x.cuda()).cpu().numpy()
+    rows = x.double().numpy().reshape(-1, 2 * N)
+    ref = O.iir_symmetric(rows, b, a).reshape(y.shape)
+    for i in range(y.shape[0]):
+        assert rel_err(y[i], ref[i]) < TOL
+
+
+def test_iir_filter_inplace_and_general_order(fbp):
+    N = 128
+    b = [0.11, -0.05, -0.04, -0.015, -0.005]            # M = 5
+    a = [-0.9, 0.2, -0.05, 0.01]                        # Q = 4 (stable)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    x = P.random_linogram(N, 1, seed=5, scale=3.0)
+    xd = x.cuda()
+    y = plan.iir_filter(xd, out=xd).cpu().numpy()       # in place
+    ref = O.iir_symmetric(x.double().numpy().reshape(-1, 2 * N), b, a).reshape(y.shape)
+    assert rel_err(y, ref) < TOL
+
+
+# --------------------------------------------------------------- end to end
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_reconstruct_configs(fbp, cfg):
+    N = P.CONFIGS[cfg]["N"]
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    S = P.make_slice(cfg, 0)
+    img = plan.reconstruct(S.cuda()).cpu().numpy()[0]
+    ref = O.reconstruct(S.double().numpy(), b, a)
+    assert rel_err(img, ref) < TOL
+
+
+@pytest.mark.parametrize("N,B,variant", [(32, 5, "spec"), (128, 3, "dc0"), (256, 2, "spec")])
+def test_reconstruct_random_batches(fbp, N, B, variant):
+    b, a = coeffs(N, variant)
+    plan = fbp.Plan(N, b, a, max_batch=B)
+    S = P.random_linogram(N, B, seed=N + B, scale=50.0)
+    img = plan.reconstruct(S.cuda()).cpu().numpy()
+    for i in range(B):
+        ref = O.reconstruct(S[i].double().numpy(), b, a)
+        assert rel_err(img[i], ref) < TOL, i
+
+
+def _sampled_check(img, S, b, a, n_pts=24, seed=0):
+    """Full-size parity on sampled pixels: oracle IIR on every row, then each sampled
+    pixel as the direct dyadic-line sum of the four families (Eq.19-22), w = 1/N."""
+    N = S.shape[1]
+    F = O.iir_symmetric(S.astype(np.float64), b, a)
+    rng = np.random.default_rng(seed)
+    pts = [(0, 0), (N // 2, N // 2), (N - 1, 0)] + [tuple(rng.integers(0, N, 2)) for _ in range(n_pts)]
+    ref = []
+    for (y, x) in pts:
+        v = (O.backproject_pixel(F, 0, y, x) + O.backproject_pixel(F, 1, y, N - 1 - x)) + \
+            (O.backproject_pixel(F, 2, x, y) + O.backproject_pixel(F, 3, x, N - 1 - y))
+        ref.append(v / N)
+    got = np.array([img[y, x] for (y, x) in pts], dtype=np.float64)
+    return got, np.array(ref)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_reconstruct_full_size(fbp, cfg):
+    """Full BASELINE sizes in the bench's launch configuration (batch of slices):
+    slice 0 compared over the whole image with the full oracle; slice 1 on sampled
+    pixels summed one by one along their dyadic lines, against the oracle peak."""
+    N = P.CONFIGS[cfg]["N"]
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    S = P.make_batch(cfg, 2, device="cuda")
+    img = plan.reconstruct(S).cpu().numpy()
+    ref0 = O.reconstruct(S[0].cpu().double().numpy(), b, a)
+    assert rel_err(img[0], ref0) < TOL
+    got, ref = _sampled_check(img[1], S[1].cpu().numpy(), b, a, seed=1)
+    assert np.max(np.abs(got - ref)) <= TOL * np.max(np.abs(ref0))
+
+
+def test_reconstruct_full_size_config5(fbp):
+    N = 4096
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    S = P.make_slice(5, 0, device="cuda").unsqueeze(0)
+    img = plan.reconstruct(S).cpu().numpy()[0]
+    ref = O.reconstruct(S[0].cpu().double().numpy(), b, a)
+    assert rel_err(img, ref) < TOL
+
+
+# ------------------------------------------------------------------- contract
+def test_determinism_and_host_path(fbp):
+    N = 256
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=3)
+    S = P.make_batch(2, 3, N=N)
+    d1 = plan.reconstruct(S.cuda()).cpu()
+    d2 = plan.reconstruct(S.cuda()).cpu()
+    assert torch.equal(d1, d2)
+    h = plan.reconstruct_host(S.numpy())
+    assert np.array_equal(h, d1.numpy())
+    hp = plan.reconstruct_host(S.pin_memory())
+    assert torch.equal(hp, d1)
+    # the separate entry points compose to the same result
+    F = plan.iir_filter(S.cuda())
+    bp = plan.backproject(F, scale=1.0 / N).cpu()
+    assert rel_err(bp.numpy(), d1.numpy()) < 1e-6
+
+
+def test_batch_edge_cases(fbp):
+    N = 64
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    S = P.random_linogram(N, 3, seed=1).cuda()
+    with pytest.raises(fbp.FbpError):
+        plan.reconstruct(S)                                  # batch 3 > max_batch 2
+    out = torch.zeros((0, N, N), device="cuda")
+    plan.reconstruct(S[:0], out=out)                         # empty batch: no-op
+    flat = torch.zeros(4 * N * 2 * N + 1, device="cuda")
+    mis = flat[1:].view(1, 4, N, 2 * N)                      # 4-byte aligned only
+    with pytest.raises(fbp.FbpError):
+        plan.reconstruct(mis)
+    assert plan.launch_count() >= 0
+
+
+def test_zero_input(fbp):
+    N = 128
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a)
+    img = plan.reconstruct(torch.zeros((1, 4, N, 2 * N), device="cuda"))
+    assert torch.count_nonzero(img) == 0

@@ -161,6 +161,8 @@ def test_dyadic_table_N8_golden():
 def test_dyadic_properties(N):
     d = O.dyadic_offsets(N)
     assert np.array_equal(d, O.dyadic_offsets_closed_form(N))
+    for y in range(N):
+        assert np.array_equal(d[:, y], O.dyadic_offsets_column(N, y))
     assert np.array_equal(d, d.T)                       # d_t(y) = d_y(t)  (R5)
     assert np.all(d[:, 0] == 0)
     assert np.array_equal(d[:, N - 1], np.arange(N))     # pattern ends at shift t
