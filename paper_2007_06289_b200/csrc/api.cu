@@ -22,6 +22,7 @@ struct fbp_plan {
   int group = 1;            // slices per workspace group
   float* F = nullptr;       // filtered linogram workspace [group][4][N][2N]
   float* R = nullptr;       // pass-A output workspace [group][4][NB][H][WR]
+  float* lane_mats = nullptr;  // [32][8*8] A^(L*j) for the IIR cross-warp carries
   size_t F_bytes = 0, R_bytes = 0;
   // host-path staging (allocated lazily by fbp_reconstruct_host)
   float* d_in[2] = {nullptr, nullptr};
@@ -105,12 +106,12 @@ Geometry make_geometry(int N, int qm) {
   g.m = n - g.k1;
   g.H = 1 << g.k1;
   g.NB = 1 << g.m;
-  g.WR = N + g.NB;
-  g.XA = std::min(128, g.W);
-  while (g.XA > 16 && (size_t)2 * g.H * (g.XA + g.H - 1) * 4 > 200 * 1024) g.XA /= 2;
-  g.XB = std::min(128, N);
-  while (g.XB > 16 && (size_t)4 * g.NB * (g.XB + g.NB - 1) * 4 > 200 * 1024) g.XB /= 2;
-  g.L = (g.W >= 32) ? g.W / 32 : 1;
+  g.WR = (N + g.NB + 3) / 4 * 4;
+  g.XA = std::max(8, std::min(128, g.W));
+  while (g.XA > 8 && fht_pass_a_smem(g) > 220 * 1024) g.XA /= 2;
+  g.XB = std::max(8, std::min(128, N));
+  while (g.XB > 8 && fht_pass_b_smem(g) > 220 * 1024) g.XB /= 2;
+  g.L = (g.W >= 1024) ? 32 : (g.W >= 32 ? g.W / 32 : 1);
   g.iir_qm = qm;
   return g;
 }
@@ -180,8 +181,8 @@ cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, in
   for (int s0 = 0; s0 < batch; s0 += p->group) {
     const int ns = std::min(p->group, batch - s0);
     cudaError_t e = timed(p, 0, st, [&] {
-      return launch_iir_rows(sino + s0 * lin_elems, p->F, (long long)ns * 4 * g.N, g, p->iir, st,
-                             launches);
+      return launch_iir_rows(sino + s0 * lin_elems, p->F, (long long)ns * 4 * g.N, g, p->iir,
+                             p->lane_mats, st, launches);
     });
     if (e != cudaSuccess) return e;
     e = run_backproject(p, p->F, img + s0 * img_elems, ns, w, st, launches);
@@ -260,10 +261,24 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   }
   std::vector<double> A, Pk;
   companion(qm, apad.data(), A);
+  auto put = [qm](float* dst, const std::vector<double>& M) {
+    for (int i = 0; i < qm; ++i)
+      for (int j = 0; j < qm; ++j) dst[i * kMaxOrder + j] = (float)M[(size_t)i * qm + j];
+  };
   for (int k = 0; k < kScanSteps; ++k) {
     matpow(qm, A, (long long)p->g.L << k, Pk);
-    for (int i = 0; i < qm; ++i)
-      for (int j = 0; j < qm; ++j) p->iir.P[k][i * kMaxOrder + j] = (float)Pk[(size_t)i * qm + j];
+    put(p->iir.P[k], Pk);
+  }
+  matpow(qm, A, 32LL * p->g.L, Pk);
+  put(p->iir.AW, Pk);
+  for (int i = 0; i < 32; ++i) {   // g_m[i] = (A^(i+1))_{0m}
+    matpow(qm, A, i + 1, Pk);
+    for (int m2 = 0; m2 < qm; ++m2) p->iir.G[i][m2] = (float)Pk[(size_t)m2];
+  }
+  std::vector<float> lm((size_t)32 * kMaxOrder * kMaxOrder, 0.0f);
+  for (int j = 0; j < 32; ++j) {
+    matpow(qm, A, (long long)p->g.L * j, Pk);
+    put(lm.data() + (size_t)j * kMaxOrder * kMaxOrder, Pk);
   }
 
   // ---- workspace, sized for a group of slices ----
@@ -277,13 +292,15 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   p->group = (int)grp;
   p->F_bytes = f_slice * p->group;
   p->R_bytes = r_slice * p->group;
-  if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess) {
+  if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess ||
+      cudaMalloc(&p->lane_mats, lm.size() * sizeof(float)) != cudaSuccess) {
     cudaGetLastError();
     fbp_plan_destroy(p);
     return fail(FBP_ERR_NOMEM, "workspace allocation failed");
   }
   // Entries of R that pass A never writes are read (and discarded) by pass B.
-  cudaError_t e = cudaMemset(p->R, 0, p->R_bytes);
+  cudaError_t e = cudaMemcpy(p->lane_mats, lm.data(), lm.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(p->R, 0, p->R_bytes);
   if (e != cudaSuccess) {
     fbp_plan_destroy(p);
     return cuda_fail(e, "cudaMemset");
@@ -302,6 +319,7 @@ void fbp_plan_destroy(fbp_plan* p) {
   DeviceGuard guard(p->device);
   cudaFree(p->F);
   cudaFree(p->R);
+  cudaFree(p->lane_mats);
   for (int i = 0; i < 2; ++i) {
     cudaFree(p->d_in[i]);
     cudaFree(p->d_out[i]);
@@ -327,7 +345,7 @@ fbp_status fbp_iir_filter(const fbp_plan* p, const float* sino, float* filtered,
   int launches = 0;
   cudaError_t e = timed(p, 0, (cudaStream_t)stream, [&] {
     return launch_iir_rows(sino, filtered, (long long)batch * 4 * p->g.N, p->g, p->iir,
-                           (cudaStream_t)stream, &launches);
+                           p->lane_mats, (cudaStream_t)stream, &launches);
   });
   p->launches = launches;
   if (e != cudaSuccess) return cuda_fail(e, "fbp_iir_filter");

@@ -17,11 +17,15 @@ constexpr int kScanSteps = 5;      // log2(32): warp-level carry scan
 // to the kernel's compile-time order QM (exact: zero taps add nothing).
 // P[k] = A^(L*2^k) (companion matrix of A, state (y[n], y[n-1], ...)) for the
 // exact chunked scan of the recursion across the 32 lanes of a warp.
+// G[i][m] = (A^(i+1))_{0m}: response of y[start+i] to the carry-in state, i < 32.
+// AW = A^(32 L): one warp of chunks.
 struct IirParams {
   float beta;
   float c[kMaxOrder];
   float a[kMaxOrder];
   float P[kScanSteps][kMaxOrder * kMaxOrder];
+  float AW[kMaxOrder * kMaxOrder];
+  float G[32][kMaxOrder];
 };
 
 struct Geometry {
@@ -35,13 +39,17 @@ struct Geometry {
   int WR;      // N + NB: compact pass-A output row width
   int XA;      // pass-A u-tile width
   int XB;      // pass-B x-tile width
-  int L;       // IIR lane chunk length (W / 32, or 1 when W < 32)
+  int L;       // IIR per-thread chunk: 32 if W >= 1024, else W/32 (1 if W < 32)
   int iir_qm;  // compile-time padded order used by the IIR kernel (3 or 8)
 };
 
 // Kernel launchers (kernels.cu).  All asynchronous on `st`; return the launch error.
+// lane_mats: device [32][8*8], lane_mats[j] = A^(L*j).
 cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const Geometry& g,
-                            const IirParams& p, cudaStream_t st, int* launches);
+                            const IirParams& p, const float* lane_mats, cudaStream_t st,
+                            int* launches);
+size_t fht_pass_a_smem(const Geometry& g);
+size_t fht_pass_b_smem(const Geometry& g);
 cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, const Geometry& g,
                               cudaStream_t st, int* launches);
 cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, float scale,

@@ -1,0 +1,392 @@
+// K2/K3: Fast Hough Transform back projection (§4.4, 251-265 §4.5
+// Eq.19-22), negative shift direction, additions only.
+//
+// Level recursion (h -> 2h):  R_2h[b][y'][u] = R_h[2b][y'/2][u] + R_h[2b+1][y'/2][u - ceil(y'/2)].
+// Radix-2^R step: after l levels (blocks of 2^l rows, row = block*2^l + c), R more
+// levels combine 2^R consecutive blocks; by d_y(t) = c*b' + d^(R)_{r'}(b') + ... :
+//   out[G*2^(l+R) + c*2^R + r'][u] = sum_{b'<2^R} in[(G*2^R + b')*2^l + c][u - c*b' - d^(R)_{r'}(b')]
+// i.e. a pre-shift c*b' of each input row (addressing only) followed by an R-level
+// FHT with compile-time shifts, done in registers on 2^R rows x 8 columns
+// (+ 2^R - 1 halo columns).  Shared-memory tiles use a padded layout
+// (col + col/8) so that lanes working on consecutive 8-column chunks are
+// bank-conflict free.
+//
+//   pass A (k_fht_a): k1 levels on each block of H = 2^k1 rows of the filtered
+//     linogram, tile = H rows x (XA core + H halo) columns; output stored compactly
+//     and only where pass B reads it (u in [N - b(c+1), 2N - c b)).
+//   pass B (k_fht_b): per channel c, rows b of G_c[b][v] = R_A[b][c][v - c b],
+//     m levels, then the family pair of Eq.22 (mirror) and the weight.
+#include "fbp_internal.h"
+
+namespace fbp {
+
+namespace {
+
+constexpr int kC = 8;  // output columns per register item
+
+__device__ __forceinline__ int pcol(int col) { return col + (col >> 3); }
+
+// Register FHT on 2^R rows: v[b][t], t in [0, kC + 2^R - 1); natural recursion,
+// shifts are compile-time.  Result row r' in v[r'].
+template <int R>
+__device__ __forceinline__ void local_fht(float (&v)[1 << R][kC + (1 << R) - 1]) {
+  constexpr int NR = 1 << R;
+  constexpr int T = kC + NR - 1;
+#pragma unroll
+  for (int lvl = 0; lvl < R; ++lvl) {
+    const int h = 1 << lvl;
+    float w[NR][T];
+#pragma unroll
+    for (int y = 0; y < NR; ++y) {
+      const int blk = y & ~(2 * h - 1);
+      const int yp = y - blk;
+      const int lo = yp >> 1;
+      const int sh = (yp + 1) >> 1;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float bv = (t >= sh) ? v[blk + h + lo][t - sh] : 0.0f;
+        w[y][t] = v[blk + lo][t] + bv;
+      }
+    }
+#pragma unroll
+    for (int y = 0; y < NR; ++y)
+#pragma unroll
+      for (int t = 0; t < T; ++t) v[y][t] = w[y][t];
+  }
+}
+
+// Load the 2^R pre-shifted input rows of item (G, c, chunk j) from a padded tile.
+// Column col_lo = j*kC - (2^R - 1); input row b' read at col - c*b'.
+template <int R>
+__device__ __forceinline__ void load_item(const float* tile, int P, int l, int G, int c, int col0,
+                                          float (&v)[1 << R][kC + (1 << R) - 1]) {
+  constexpr int NR = 1 << R;
+  constexpr int T = kC + NR - 1;
+#pragma unroll
+  for (int b = 0; b < NR; ++b) {
+    const int row = ((G << R) + b) * (1 << l) + c;
+    const float* rp = tile + (size_t)row * P;
+    const int cs = col0 - (NR - 1) - c * b;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int col = cs + t;
+      v[b][t] = (col >= 0) ? rp[pcol(col)] : 0.0f;
+    }
+  }
+}
+
+// One radix step in shared memory: tiles in -> out (padded, pitch P), items over
+// output chunks [chunk0, chunk0 + nchunks).
+template <int R>
+__device__ void radix_step_smem(const float* in, float* out, int P, int rows, int l, int chunk0,
+                                int nchunks) {
+  constexpr int NR = 1 << R;
+  const int nch = 1 << l;                  // channels
+  const int ngroups = rows >> (l + R);
+  const int items = ngroups * nch * nchunks;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int j = chunk0 + it % nchunks;
+    const int gc = it / nchunks;
+    const int c = gc % nch;
+    const int G = gc / nch;
+    float v[NR][kC + NR - 1];
+    load_item<R>(in, P, l, G, c, j * kC, v);
+    local_fht<R>(v);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      float* op = out + (size_t)((G << (l + R)) + c * NR + r) * P;
+#pragma unroll
+      for (int t = 0; t < kC; ++t) op[pcol(j * kC + t)] = v[r][NR - 1 + t];
+    }
+  }
+}
+
+__device__ __forceinline__ void radix_step_dispatch(int R, const float* in, float* out, int P,
+                                                    int rows, int l, int chunk0, int nchunks) {
+  if (R == 3) radix_step_smem<3>(in, out, P, rows, l, chunk0, nchunks);
+  else if (R == 2) radix_step_smem<2>(in, out, P, rows, l, chunk0, nchunks);
+  else radix_step_smem<1>(in, out, P, rows, l, chunk0, nchunks);
+}
+
+// Split `levels` into radix steps of at most 3 levels: returns the radix of step s.
+__device__ __forceinline__ int step_radix(int levels, int s) {
+  // 1->[1] 2->[2] 3->[3] 4->[2,2] 5->[3,2] 6->[3,3] 7->[3,2,2] 8->[3,3,2]
+  const int nsteps = (levels + 2) / 3;
+  const int base = levels / nsteps, extra = levels % nsteps;
+  return base + (s < extra ? 1 : 0);
+}
+
+// Run all levels of a pass on a tile whose first buffer is `a`; the last radix step
+// is NOT executed (the caller fuses it with its epilogue).  Returns the buffer
+// holding the input of the last step and sets *l_last, *R_last.
+__device__ __forceinline__ float* run_levels_but_last(float* a, float* b, int P, int rows,
+                                                      int levels, int nchunks_all, int* l_last,
+                                                      int* R_last) {
+  const int nsteps = (levels + 2) / 3;
+  int l = 0;
+  for (int s = 0; s < nsteps - 1; ++s) {
+    const int R = step_radix(levels, s);
+    radix_step_dispatch(R, a, b, P, rows, l, 0, nchunks_all);
+    __syncthreads();
+    float* t = a;
+    a = b;
+    b = t;
+    l += R;
+  }
+  *l_last = l;
+  *R_last = (nsteps > 0) ? step_radix(levels, nsteps - 1) : 0;
+  return a;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Pass A.  grid (ceil(W/XA) tiles, NB blocks, slices*4), block 256.
+// Tile columns u in [u0 - Hp, u0 + XA) -> local col = u - u0 + Hp  (Hp = H rounded
+// up to 8 so the core starts on a chunk boundary); F outside [0, W) reads as 0.
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp, int l, int XA,
+                                                 int u0, int b, const Geometry& g, float* dstR) {
+  constexpr int NR = 1 << R;
+  const int nch = 1 << l;
+  const int nchunks = XA / kC;
+  const int chunk0 = Hp / kC;
+  const int items = nch * nchunks;   // a single group in the last step
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int j = chunk0 + it % nchunks;
+    const int c = it / nchunks;
+    float v[NR][kC + NR - 1];
+    load_item<R>(in, P, l, 0, c, j * kC, v);
+    local_fht<R>(v);
+    const int ubase = u0 - Hp + j * kC;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int cf = c * NR + r;                 // final pass-A channel
+      const int ulo = g.N - b * (cf + 1);
+      const int uhi = g.W - cf * b;
+      float* out = dstR + (long long)cf * g.WR + (cf * b - g.N + g.NB);
+      if (ubase >= ulo && ubase + kC <= uhi) {
+#pragma unroll
+        for (int t = 0; t < kC; ++t) out[ubase + t] = v[r][NR - 1 + t];
+      } else {
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          const int u = ubase + t;
+          if (u >= ulo && u < uhi) out[u] = v[r][NR - 1 + t];
+        }
+      }
+    }
+  }
+}
+
+// Fill `rows` x D padded tile rows from global rows (pitch gp) starting at global
+// column g0 (may be negative); columns outside [0, gw) read as 0.
+__device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, const float* src,
+                                          long long gp, int g0, int gw) {
+  const int q4 = D >> 2;
+  const bool vec = ((g0 & 3) == 0) && ((gp & 3) == 0);
+  for (int e = threadIdx.x; e < rows * q4; e += blockDim.x) {
+    const int r = e / q4;
+    const int c4 = (e - r * q4) * 4;
+    const int u = g0 + c4;
+    const float* rp = src + (long long)r * gp;
+    float4 v;
+    if (vec && u >= 0 && u + 3 < gw) {
+      v = __ldg(reinterpret_cast<const float4*>(rp + u));
+    } else {
+      v.x = (u >= 0 && u < gw) ? rp[u] : 0.0f;
+      v.y = (u + 1 >= 0 && u + 1 < gw) ? rp[u + 1] : 0.0f;
+      v.z = (u + 2 >= 0 && u + 2 < gw) ? rp[u + 2] : 0.0f;
+      v.w = (u + 3 >= 0 && u + 3 < gw) ? rp[u + 3] : 0.0f;
+    }
+    float* d = tile + (size_t)r * P + pcol(c4);
+    d[0] = v.x;
+    d[1] = v.y;
+    d[2] = v.z;
+    d[3] = v.w;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fht_a(const float* __restrict__ lin,
+                                               float* __restrict__ R, Geometry g, int P) {
+  extern __shared__ float smem[];
+  const int b = blockIdx.y;
+  const long long sf = blockIdx.z;
+  const int XA = g.XA, H = g.H;
+  const int Hp = (H + kC - 1) / kC * kC;
+  const int u0 = blockIdx.x * XA;
+  if (u0 + XA <= g.N - b * H) return;      // no channel needs these columns
+  const int D = XA + Hp;
+  float* A = smem;
+  float* B = smem + (size_t)H * P;
+  const float* src = lin + (sf * g.N + (long long)b * H) * g.W;
+  fill_tile(A, P, H, D, src, g.W, u0 - Hp, g.W);
+  __syncthreads();
+  int l_last, R_last;
+  const float* in = run_levels_but_last(A, B, P, H, g.k1, D / kC, &l_last, &R_last);
+  float* dstR = R + ((sf * g.NB + b) * (long long)H) * g.WR;
+  if (R_last == 3) pass_a_last_step<3>(in, P, Hp, l_last, XA, u0, b, g, dstR);
+  else if (R_last == 2) pass_a_last_step<2>(in, P, Hp, l_last, XA, u0, b, g, dstR);
+  else pass_a_last_step<1>(in, P, Hp, l_last, XA, u0, b, g, dstR);
+}
+
+// ---------------------------------------------------------------------------
+// Pass B.  grid (ceil(N/XB) x-tiles, H channels, slices), block 256.
+// Family f = 2*pair + q at tile start xs (q = 0: x0; q = 1: mirrored N - x0 - XB).
+// Rows b in [0,NB) of G_c[b][v], v in [u0 - NBp, u0 + XB), u0 = xs + N; compact R
+// index j' = v - N + NB.  Family 1 runs first and is parked in smem; family 0 then
+// adds the mirrored values (Eq.22 pair), scales and stores.
+// ---------------------------------------------------------------------------
+template <int R, bool PARK>
+__device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp, int l, int XB,
+                                                 float* park, const float* parked, float* out,
+                                                 int pair, int c, int NB, int x0, float scale,
+                                                 int N) {
+  constexpr int NR = 1 << R;
+  const int nch = 1 << l;
+  const int nchunks = XB / kC;
+  const int items = nch * nchunks;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int jj = it % nchunks;
+    const int cc = it / nchunks;
+    float v[NR][kC + NR - 1];
+    load_item<R>(in, P, l, 0, cc, NBp + jj * kC, v);
+    local_fht<R>(v);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int rf = cc * NR + r;               // final row within the channel block
+      if (PARK) {
+#pragma unroll
+        for (int t = 0; t < kC; ++t) park[rf * XB + jj * kC + t] = v[r][NR - 1 + t];
+      } else {
+        float s[kC];
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          const int i = jj * kC + t;
+          s[t] = scale * (v[r][NR - 1 + t] + parked[rf * XB + (XB - 1 - i)]);
+        }
+        const int y = c * NB + rf;
+        const int xb = x0 + jj * kC;
+        if (pair == 0) {
+          float* o = out + (long long)y * N + xb;
+          if (xb + kC <= N) {
+            *reinterpret_cast<float4*>(o) = make_float4(s[0], s[1], s[2], s[3]);
+            *reinterpret_cast<float4*>(o + 4) = make_float4(s[4], s[5], s[6], s[7]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < kC; ++t)
+              if (xb + t < N) o[t] = s[t];
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < kC; ++t) {
+            if (xb + t < N) {
+              float* o = out + (long long)(xb + t) * N + y;
+              *o = *o + s[t];
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool PARK>
+__device__ __forceinline__ void pass_b_last(int R, const float* in, int P, int NBp, int l, int XB,
+                                            float* park, const float* parked, float* out, int pair,
+                                            int c, int NB, int x0, float scale, int N) {
+  if (R == 3) pass_b_last_step<3, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
+  else if (R == 2) pass_b_last_step<2, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
+  else pass_b_last_step<1, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
+}
+
+__global__ void __launch_bounds__(256) k_fht_b(const float* __restrict__ R,
+                                               float* __restrict__ img, Geometry g, int P,
+                                               int pair, float scale) {
+  extern __shared__ float smem[];
+  const int NB = g.NB, XB = g.XB, N = g.N;
+  const int NBp = (NB + kC - 1) / kC * kC;
+  const int c = blockIdx.y;
+  const long long slice = blockIdx.z;
+  const int x0 = blockIdx.x * XB;
+  const int D = XB + NBp;
+  float* A = smem;
+  float* B = smem + (size_t)NB * P;
+  float* park = B + (size_t)NB * P;       // [NB][XB]
+  float* out = img + slice * (long long)N * N;
+  for (int q = 1; q >= 0; --q) {
+    const int f = 2 * pair + q;
+    const int xs = (q == 0) ? x0 : (N - x0 - XB);
+    const float* src = R + (((slice * 4 + f) * NB) * (long long)g.H + c) * g.WR;
+    fill_tile(A, P, NB, D, src, (long long)g.H * g.WR, xs - NBp + NB, g.WR);
+    __syncthreads();
+    int l_last = 0, R_last = 0;
+    const float* in = A;
+    if (g.m > 0) in = run_levels_but_last(A, B, P, NB, g.m, D / kC, &l_last, &R_last);
+    if (g.m == 0) {
+      // NB == 1: the single row is the result (no levels)
+      for (int i = threadIdx.x; i < XB; i += blockDim.x) {
+        const float v = in[pcol(NBp + i)];
+        if (q == 1) {
+          park[i] = v;
+        } else if (x0 + i < N) {
+          const float sv = scale * (v + park[XB - 1 - i]);
+          if (pair == 0) out[(long long)c * N + x0 + i] = sv;
+          else { float* o = out + (long long)(x0 + i) * N + c; *o = *o + sv; }
+        }
+      }
+    } else if (q == 1) {
+      pass_b_last<true>(R_last, in, P, NBp, l_last, XB, park, nullptr, out, pair, c, NB, x0, scale, N);
+    } else {
+      pass_b_last<false>(R_last, in, P, NBp, l_last, XB, nullptr, park, out, pair, c, NB, x0, scale, N);
+    }
+    __syncthreads();
+  }
+}
+
+static int pitch_for(int D) {
+  int P = D + (D >> 3) + 1;
+  if ((P & 1) == 0) ++P;
+  return P;
+}
+
+size_t fht_pass_a_smem(const Geometry& g) {
+  const int Hp = (g.H + kC - 1) / kC * kC;
+  return (size_t)2 * g.H * pitch_for(g.XA + Hp) * sizeof(float);
+}
+
+size_t fht_pass_b_smem(const Geometry& g) {
+  const int NBp = (g.NB + kC - 1) / kC * kC;
+  return ((size_t)2 * g.NB * pitch_for(g.XB + NBp) + (size_t)g.NB * g.XB) * sizeof(float);
+}
+
+cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, const Geometry& g,
+                              cudaStream_t st, int* launches) {
+  if (slices <= 0) return cudaSuccess;
+  const int Hp = (g.H + kC - 1) / kC * kC;
+  const int P = pitch_for(g.XA + Hp);
+  const size_t smem = fht_pass_a_smem(g);
+  cudaError_t e = cudaFuncSetAttribute(k_fht_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((g.W + g.XA - 1) / g.XA, g.NB, slices * 4);
+  k_fht_a<<<grid, 256, smem, st>>>(lin, R, g, P);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, float scale,
+                              const Geometry& g, cudaStream_t st, int* launches) {
+  if (slices <= 0) return cudaSuccess;
+  const int NBp = (g.NB + kC - 1) / kC * kC;
+  const int P = pitch_for(g.XB + NBp);
+  const size_t smem = fht_pass_b_smem(g);
+  cudaError_t e = cudaFuncSetAttribute(k_fht_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((g.N + g.XB - 1) / g.XB, g.H, slices);
+  k_fht_b<<<grid, 256, smem, st>>>(R, img, g, P, pair, scale);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace fbp

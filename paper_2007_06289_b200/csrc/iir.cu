@@ -1,0 +1,291 @@
+// K1 k_iir: symmetric recursive ramp filter of every linogram row
+// (§3 Eq.12-13; per-direction feedback R10, zero state and zero
+// extension R11; difference-form feedforward R16).
+//
+// One CTA per row (W = 2N samples); thread i owns the contiguous chunk
+// [i*L, i*L + L) in registers (L = 32 when W >= 1024).  Exact chunked scan:
+//   1. zero-state sweeps of the chunk, causal then anticausal, from registers:
+//      local outputs y_loc = y+_loc + y-_loc and the chunk end states v+, v-;
+//   2. inclusive scan of the end states over threads, c_i = A^L c_{i-1} + v_i
+//      (warp Kogge-Stone with A^(L 2^k), then the warp aggregates combined with
+//      A^(32 L) and injected with A^(L (lane+1)));
+//   3. fix-up with the exact carry-in c (homogeneous response of the recursion):
+//      y[i] = y_loc[i] + sum_m g_m[i] c+_m + sum_m g_m[L-1-i] c-_m,
+//      g_m[i] = (A^(i+1))_{0m}.
+// Global traffic: the row is read once (coalesced, float4) and written once.
+#include "fbp_internal.h"
+
+namespace fbp {
+
+namespace {
+
+__device__ __forceinline__ int pad_idx(int s) { return s + ((s >> 5) << 2); }  // +4 floats per 32
+
+template <int QM>
+__device__ __forceinline__ void matvec_acc(const float* M, const float (&v)[QM], float (&acc)[QM]) {
+#pragma unroll
+  for (int i = 0; i < QM; ++i) {
+    float s = acc[i];
+#pragma unroll
+    for (int j = 0; j < QM; ++j) s = fmaf(M[i * kMaxOrder + j], v[j], s);
+    acc[i] = s;
+  }
+}
+
+}  // namespace
+
+template <int QM, int L, bool BETA>
+__global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
+                                             const float* __restrict__ lane_mats, IirParams p) {
+  extern __shared__ float sm[];
+  float* row_s = sm;                                   // W * 36/32 floats (padded)
+  float* wagg = sm + (W / 32) * 36 + 64;               // [2][nwarps][QM] warp aggregates
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int nwarps = nthr >> 5;
+  const long long row = blockIdx.x;
+  const float* src = in + row * (long long)W;
+  float* dst = out + row * (long long)W;
+
+  // ---- coalesced load of the row into padded shared memory ----
+  if (W >= 4) {
+    for (int s = 4 * tid; s < W; s += 4 * nthr) {
+      const float4 v = *reinterpret_cast<const float4*>(src + s);
+      *reinterpret_cast<float4*>(row_s + pad_idx(s)) = v;
+    }
+  } else {
+    for (int s = tid; s < W; s += nthr) row_s[pad_idx(s)] = src[s];
+  }
+  __syncthreads();
+
+  const int start = tid * L;
+  const bool active = start < W;
+  float x[L];
+  float y[L];
+  float xl[QM + 1], xr[QM + 1];  // x[start-1-k], x[start+L+k]
+#pragma unroll
+  for (int k = 0; k <= QM; ++k) {
+    const int sl = start - 1 - k, sr = start + L + k;
+    xl[k] = (active && sl >= 0) ? row_s[pad_idx(sl)] : 0.0f;
+    xr[k] = (active && sr < W) ? row_s[pad_idx(sr)] : 0.0f;
+  }
+  if (L % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < L; i += 4) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (active) v = *reinterpret_cast<const float4*>(row_s + pad_idx(start + i));
+      x[i] = v.x;
+      x[i + 1] = v.y;
+      x[i + 2] = v.z;
+      x[i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < L; ++i) x[i] = active ? row_s[pad_idx(start + i)] : 0.0f;
+  }
+
+  // ---- 1a. causal zero-state sweep:  u = beta x + sum_k c_k D[n-k], D[n] = x[n]-x[n-1] ----
+  float vc[QM];
+  {
+    float dh[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) dh[k] = xl[k] - xl[k + 1];
+    float yq[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) yq[k] = 0.0f;
+    float xprev = xl[0];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const float d = x[i] - xprev;
+      xprev = x[i];
+      float u = BETA ? p.beta * x[i] : 0.0f;
+      u = fmaf(p.c[0], d, u);
+#pragma unroll
+      for (int k = 1; k < QM; ++k) u = fmaf(p.c[k], dh[k - 1], u);
+#pragma unroll
+      for (int k = QM - 1; k > 0; --k) dh[k] = dh[k - 1];
+      dh[0] = d;
+      float v = u;
+#pragma unroll
+      for (int k = QM - 1; k >= 0; --k) v = fmaf(-p.a[k], yq[k], v);
+#pragma unroll
+      for (int k = QM - 1; k > 0; --k) yq[k] = yq[k - 1];
+      yq[0] = v;
+      y[i] = v;
+    }
+#pragma unroll
+    for (int k = 0; k < QM; ++k) vc[k] = active ? yq[k] : 0.0f;
+  }
+  // ---- 1b. anticausal zero-state sweep:  u = beta x + sum_k c_k E[n+k], E[n] = x[n]-x[n+1] ----
+  float va[QM];
+  {
+    float eh[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) eh[k] = xr[k] - xr[k + 1];
+    float yq[QM];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) yq[k] = 0.0f;
+    float xnext = xr[0];
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      const float e = x[i] - xnext;
+      xnext = x[i];
+      float u = BETA ? p.beta * x[i] : 0.0f;
+      u = fmaf(p.c[0], e, u);
+#pragma unroll
+      for (int k = 1; k < QM; ++k) u = fmaf(p.c[k], eh[k - 1], u);
+#pragma unroll
+      for (int k = QM - 1; k > 0; --k) eh[k] = eh[k - 1];
+      eh[0] = e;
+      float v = u;
+#pragma unroll
+      for (int k = QM - 1; k >= 0; --k) v = fmaf(-p.a[k], yq[k], v);
+#pragma unroll
+      for (int k = QM - 1; k > 0; --k) yq[k] = yq[k - 1];
+      yq[0] = v;
+      y[i] += v;
+    }
+#pragma unroll
+    for (int k = 0; k < QM; ++k) va[k] = active ? yq[k] : 0.0f;
+  }
+
+  // ---- 2. scans of the chunk states across threads ----
+  // causal: inclusive over lanes (ascending), warp aggregates in lane 31
+#pragma unroll
+  for (int k = 0; k < kScanSteps; ++k) {
+    const int off = 1 << k;
+    float oc[QM], oa[QM];
+#pragma unroll
+    for (int j = 0; j < QM; ++j) {
+      oc[j] = __shfl_up_sync(0xffffffffu, vc[j], off);
+      oa[j] = __shfl_down_sync(0xffffffffu, va[j], off);
+    }
+    if (lane >= off) matvec_acc<QM>(p.P[k], oc, vc);
+    if (lane + off < 32) matvec_acc<QM>(p.P[k], oa, va);
+  }
+  if (nwarps > 1) {
+    if (lane == 31) {
+#pragma unroll
+      for (int j = 0; j < QM; ++j) wagg[warp * QM + j] = vc[j];
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < QM; ++j) wagg[(nwarps + warp) * QM + j] = va[j];
+    }
+  }
+  __syncthreads();
+  // exclusive carry-in per thread
+  float cc[QM], ca[QM];
+#pragma unroll
+  for (int j = 0; j < QM; ++j) {
+    const float u = __shfl_up_sync(0xffffffffu, vc[j], 1);
+    const float d = __shfl_down_sync(0xffffffffu, va[j], 1);
+    cc[j] = (lane == 0) ? 0.0f : u;
+    ca[j] = (lane == 31) ? 0.0f : d;
+  }
+  if (nwarps > 1) {
+    // warp carry-ins K (causal from the left, anticausal from the right)
+    float K[QM], Ka[QM];
+#pragma unroll
+    for (int j = 0; j < QM; ++j) K[j] = Ka[j] = 0.0f;
+    for (int w = 0; w < warp; ++w) {
+      float t[QM];
+#pragma unroll
+      for (int j = 0; j < QM; ++j) t[j] = wagg[w * QM + j];
+      float nk[QM];
+#pragma unroll
+      for (int j = 0; j < QM; ++j) nk[j] = t[j];
+      matvec_acc<QM>(p.AW, K, nk);     // K <- A^(32L) K + agg_w
+#pragma unroll
+      for (int j = 0; j < QM; ++j) K[j] = nk[j];
+    }
+    for (int w = nwarps - 1; w > warp; --w) {
+      float t[QM];
+#pragma unroll
+      for (int j = 0; j < QM; ++j) t[j] = wagg[(nwarps + w) * QM + j];
+      float nk[QM];
+#pragma unroll
+      for (int j = 0; j < QM; ++j) nk[j] = t[j];
+      matvec_acc<QM>(p.AW, Ka, nk);
+#pragma unroll
+      for (int j = 0; j < QM; ++j) Ka[j] = nk[j];
+    }
+    // thread carry-in += A^(L*lane) K  (causal),  A^(L*(31-lane)) Ka  (anticausal)
+    matvec_acc<QM>(lane_mats + (size_t)lane * kMaxOrder * kMaxOrder, K, cc);
+    matvec_acc<QM>(lane_mats + (size_t)(31 - lane) * kMaxOrder * kMaxOrder, Ka, ca);
+  }
+
+  // ---- 3. fix-up with the homogeneous responses, then store ----
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    float v = y[i];
+#pragma unroll
+    for (int m = 0; m < QM; ++m) {
+      v = fmaf(p.G[i][m], cc[m], v);
+      v = fmaf(p.G[L - 1 - i][m], ca[m], v);
+    }
+    y[i] = v;
+  }
+  __syncthreads();  // everyone has read row_s
+  if (active) {
+    if (L % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < L; i += 4)
+        *reinterpret_cast<float4*>(row_s + pad_idx(start + i)) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < L; ++i) row_s[pad_idx(start + i)] = y[i];
+    }
+  }
+  __syncthreads();
+  if (W >= 4) {
+    for (int s = 4 * tid; s < W; s += 4 * nthr)
+      *reinterpret_cast<float4*>(dst + s) = *reinterpret_cast<const float4*>(row_s + pad_idx(s));
+  } else {
+    for (int s = tid; s < W; s += nthr) dst[s] = row_s[pad_idx(s)];
+  }
+}
+
+template <int QM, int L>
+static cudaError_t launch_L(const float* in, float* out, long long rows, const Geometry& g,
+                            const IirParams& p, const float* lane_mats, cudaStream_t st) {
+  const int threads = (g.W >= 32 * L) ? g.W / L : 32;
+  const int nwarps = threads / 32;
+  const size_t smem = ((size_t)(g.W / 32 + 1) * 36 + 64 + 2 * nwarps * QM + 16) * sizeof(float);
+  const bool beta = p.beta != 0.0f;
+  auto k = beta ? k_iir<QM, L, true> : k_iir<QM, L, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  for (long long r0 = 0; r0 < rows; r0 += 2147483647LL) {
+    const long long nr = (rows - r0 < 2147483647LL) ? rows - r0 : 2147483647LL;
+    k<<<(unsigned)nr, threads, smem, st>>>(in + r0 * g.W, out + r0 * g.W, g.W, lane_mats, p);
+  }
+  return cudaGetLastError();
+}
+
+template <int QM>
+static cudaError_t launch_qm(const float* in, float* out, long long rows, const Geometry& g,
+                             const IirParams& p, const float* lane_mats, cudaStream_t st) {
+  switch (g.L) {
+    case 1: return launch_L<QM, 1>(in, out, rows, g, p, lane_mats, st);
+    case 2: return launch_L<QM, 2>(in, out, rows, g, p, lane_mats, st);
+    case 4: return launch_L<QM, 4>(in, out, rows, g, p, lane_mats, st);
+    case 8: return launch_L<QM, 8>(in, out, rows, g, p, lane_mats, st);
+    case 16: return launch_L<QM, 16>(in, out, rows, g, p, lane_mats, st);
+    default: return launch_L<QM, 32>(in, out, rows, g, p, lane_mats, st);
+  }
+}
+
+cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const Geometry& g,
+                            const IirParams& p, const float* lane_mats, cudaStream_t st,
+                            int* launches) {
+  if (rows <= 0) return cudaSuccess;
+  cudaError_t e = (g.iir_qm == 3) ? launch_qm<3>(in, out, rows, g, p, lane_mats, st)
+                                  : launch_qm<8>(in, out, rows, g, p, lane_mats, st);
+  if (launches) ++*launches;
+  return e;
+}
+
+}  // namespace fbp
