@@ -20,6 +20,7 @@ struct fbp_plan {
   int device = 0;
   int max_batch = 1;
   int group = 1;            // slices per workspace group
+  bool per_family = false;  // schedule IIR -> pass A one family at a time (large N)
   float* F = nullptr;       // filtered linogram workspace [group][4][N][2N]
   float* R = nullptr;       // pass-A output workspace [group][4][NB][H][WR]
   float* lane_mats = nullptr;  // [32][8*8] A^(L*j) for the IIR cross-warp carries
@@ -165,7 +166,10 @@ cudaError_t timed(const fbp_plan* p, int kind, cudaStream_t st, Fn&& fn) {
 // FHT back projection of `slices` linograms (device) into images, via plan->R.
 cudaError_t run_backproject(const fbp_plan* p, const float* lin, float* img, int slices,
                             float scale, cudaStream_t st, int* launches) {
-  cudaError_t e = timed(p, 1, st, [&] { return launch_fht_pass_a(lin, p->R, slices, p->g, st, launches); });
+  const long long lin_elems = 4LL * p->g.N * p->g.W;
+  cudaError_t e = timed(p, 1, st, [&] {
+    return launch_fht_pass_a(lin, p->R, slices, 0, 4, lin_elems, p->g, st, launches);
+  });
   if (e != cudaSuccess) return e;
   e = timed(p, 2, st, [&] { return launch_fht_pass_b(p->R, img, slices, 0, scale, p->g, st, launches); });
   if (e != cudaSuccess) return e;
@@ -178,6 +182,32 @@ cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, in
   const long long lin_elems = 4LL * g.N * g.W;
   const long long img_elems = (long long)g.N * g.N;
   const float w = 1.0f / (float)g.N;  // exact power of two (R7)
+  const long long fam_elems = (long long)g.N * g.W;
+  if (p->per_family) {
+    // Large N: one line family at a time, so that the filtered family (N x 2N
+    // fp32, 32 MiB at N = 2048) is consumed by pass A while it is L2-resident;
+    // pass B runs once both families of its Eq.22 pair are done.
+    for (int s = 0; s < batch; ++s) {
+      const float* S = sino + s * lin_elems;
+      for (int f = 0; f < 4; ++f) {
+        cudaError_t e = timed(p, 0, st, [&] {
+          return launch_iir_rows(S + f * fam_elems, p->F, g.N, g, p->iir, p->lane_mats, st, launches);
+        });
+        if (e != cudaSuccess) return e;
+        e = timed(p, 1, st, [&] {
+          return launch_fht_pass_a(p->F, p->R, 1, f, 1, fam_elems, g, st, launches);
+        });
+        if (e != cudaSuccess) return e;
+        if (f & 1) {
+          e = timed(p, 2, st, [&] {
+            return launch_fht_pass_b(p->R, img + s * img_elems, 1, f >> 1, w, g, st, launches);
+          });
+          if (e != cudaSuccess) return e;
+        }
+      }
+    }
+    return cudaSuccess;
+  }
   for (int s0 = 0; s0 < batch; s0 += p->group) {
     const int ns = std::min(p->group, batch - s0);
     cudaError_t e = timed(p, 0, st, [&] {
@@ -290,6 +320,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   grp = std::max<long long>(1, std::min<long long>(grp, max_batch));
   grp = std::min<long long>(grp, 16383);
   p->group = (int)grp;
+  p->per_family = (p->group == 1 && n >= 1024);
   p->F_bytes = f_slice * p->group;
   p->R_bytes = r_slice * p->group;
   if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess ||

@@ -50,8 +50,11 @@ cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const G
                             int* launches);
 size_t fht_pass_a_smem(const Geometry& g);
 size_t fht_pass_b_smem(const Geometry& g);
-cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, const Geometry& g,
-                              cudaStream_t st, int* launches);
+// Pass A over `slices` x families [f0, f0+nf): input family fi of slice s at
+// lin + s*lin_slice_stride + fi*N*W; output R[(s*4 + f0 + fi)].
+cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, int f0, int nf,
+                              long long lin_slice_stride, const Geometry& g, cudaStream_t st,
+                              int* launches);
 cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, float scale,
                               const Geometry& g, cudaStream_t st, int* launches);
 

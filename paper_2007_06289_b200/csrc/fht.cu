@@ -181,38 +181,56 @@ __device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp,
 }
 
 // Fill `rows` x D padded tile rows from global rows (pitch gp) starting at global
-// column g0 (may be negative); columns outside [0, gw) read as 0.
+// column g0 (may be negative); columns outside [0, gw) read as 0.  Each thread
+// issues kU independent float4 loads before storing (memory-level parallelism).
 __device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, const float* src,
                                           long long gp, int g0, int gw) {
+  constexpr int kU = 6;
   const int q4 = D >> 2;
+  const int total = rows * q4;
   const bool vec = ((g0 & 3) == 0) && ((gp & 3) == 0);
-  for (int e = threadIdx.x; e < rows * q4; e += blockDim.x) {
-    const int r = e / q4;
-    const int c4 = (e - r * q4) * 4;
-    const int u = g0 + c4;
-    const float* rp = src + (long long)r * gp;
-    float4 v;
-    if (vec && u >= 0 && u + 3 < gw) {
-      v = __ldg(reinterpret_cast<const float4*>(rp + u));
-    } else {
-      v.x = (u >= 0 && u < gw) ? rp[u] : 0.0f;
-      v.y = (u + 1 >= 0 && u + 1 < gw) ? rp[u + 1] : 0.0f;
-      v.z = (u + 2 >= 0 && u + 2 < gw) ? rp[u + 2] : 0.0f;
-      v.w = (u + 3 >= 0 && u + 3 < gw) ? rp[u + 3] : 0.0f;
+  for (int e0 = threadIdx.x; e0 < total; e0 += kU * blockDim.x) {
+    float4 v[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int e = e0 + k * blockDim.x;
+      if (e < total) {
+        const int r = e / q4;
+        const int u = g0 + (e - r * q4) * 4;
+        const float* rp = src + (long long)r * gp;
+        if (vec && u >= 0 && u + 3 < gw) {
+          v[k] = __ldg(reinterpret_cast<const float4*>(rp + u));
+        } else {
+          v[k].x = (u >= 0 && u < gw) ? rp[u] : 0.0f;
+          v[k].y = (u + 1 >= 0 && u + 1 < gw) ? rp[u + 1] : 0.0f;
+          v[k].z = (u + 2 >= 0 && u + 2 < gw) ? rp[u + 2] : 0.0f;
+          v[k].w = (u + 3 >= 0 && u + 3 < gw) ? rp[u + 3] : 0.0f;
+        }
+      }
     }
-    float* d = tile + (size_t)r * P + pcol(c4);
-    d[0] = v.x;
-    d[1] = v.y;
-    d[2] = v.z;
-    d[3] = v.w;
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int e = e0 + k * blockDim.x;
+      if (e < total) {
+        const int r = e / q4;
+        const int c4 = (e - r * q4) * 4;
+        float* d = tile + (size_t)r * P + pcol(c4);
+        d[0] = v[k].x;
+        d[1] = v[k].y;
+        d[2] = v[k].z;
+        d[3] = v[k].w;
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(256) k_fht_a(const float* __restrict__ lin,
-                                               float* __restrict__ R, Geometry g, int P) {
+__global__ void __launch_bounds__(256, 2) k_fht_a(const float* __restrict__ lin,
+                                               float* __restrict__ R, Geometry g, int P, int f0,
+                                               int nf, long long lin_slice_stride) {
   extern __shared__ float smem[];
   const int b = blockIdx.y;
-  const long long sf = blockIdx.z;
+  const int zs = blockIdx.z / nf, zf = blockIdx.z % nf;
+  const long long sf = (long long)zs * 4 + f0 + zf;     // output (slice, family)
   const int XA = g.XA, H = g.H;
   const int Hp = (H + kC - 1) / kC * kC;
   const int u0 = blockIdx.x * XA;
@@ -220,7 +238,7 @@ __global__ void __launch_bounds__(256) k_fht_a(const float* __restrict__ lin,
   const int D = XA + Hp;
   float* A = smem;
   float* B = smem + (size_t)H * P;
-  const float* src = lin + (sf * g.N + (long long)b * H) * g.W;
+  const float* src = lin + zs * lin_slice_stride + ((long long)zf * g.N + (long long)b * H) * g.W;
   fill_tile(A, P, H, D, src, g.W, u0 - Hp, g.W);
   __syncthreads();
   int l_last, R_last;
@@ -242,7 +260,7 @@ template <int R, bool PARK>
 __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp, int l, int XB,
                                                  float* park, const float* parked, float* out,
                                                  int pair, int c, int NB, int x0, float scale,
-                                                 int N) {
+                                                 int N, float* stage) {
   constexpr int NR = 1 << R;
   const int nch = 1 << l;
   const int nchunks = XB / kC;
@@ -279,13 +297,10 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
               if (xb + t < N) o[t] = s[t];
           }
         } else {
+          // transposed pair: park in the free tile buffer (padded rows), written
+          // out coalesced by pass_b_flush_h after the barrier
 #pragma unroll
-          for (int t = 0; t < kC; ++t) {
-            if (xb + t < N) {
-              float* o = out + (long long)(xb + t) * N + y;
-              *o = *o + s[t];
-            }
-          }
+          for (int t = 0; t < kC; ++t) stage[rf * P + pcol(jj * kC + t)] = s[t];
         }
       }
     }
@@ -295,13 +310,41 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
 template <bool PARK>
 __device__ __forceinline__ void pass_b_last(int R, const float* in, int P, int NBp, int l, int XB,
                                             float* park, const float* parked, float* out, int pair,
-                                            int c, int NB, int x0, float scale, int N) {
-  if (R == 3) pass_b_last_step<3, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
-  else if (R == 2) pass_b_last_step<2, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
-  else pass_b_last_step<1, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N);
+                                            int c, int NB, int x0, float scale, int N, float* stage) {
+  if (R == 3) pass_b_last_step<3, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
+  else if (R == 2) pass_b_last_step<2, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
+  else pass_b_last_step<1, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
 }
 
-__global__ void __launch_bounds__(256) k_fht_b(const float* __restrict__ R,
+// h pair: out[x0 + i][c*NB + r] += stage[r][i]  (stage rows padded like the tiles)
+__device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB, int XB, int c,
+                                               int x0, float* out, int N) {
+  if ((NB & 3) == 0) {
+    const int q = NB >> 2;
+    for (int e = threadIdx.x; e < XB * q; e += blockDim.x) {
+      const int i = e / q;
+      const int r = (e - i * q) * 4;
+      if (x0 + i >= N) continue;
+      float4* o = reinterpret_cast<float4*>(out + (long long)(x0 + i) * N + c * NB + r);
+      float4 v = *o;
+      v.x += stage[(r + 0) * P + pcol(i)];
+      v.y += stage[(r + 1) * P + pcol(i)];
+      v.z += stage[(r + 2) * P + pcol(i)];
+      v.w += stage[(r + 3) * P + pcol(i)];
+      *o = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < XB * NB; e += blockDim.x) {
+      const int i = e / NB;
+      const int r = e - i * NB;
+      if (x0 + i >= N) continue;
+      float* o = out + (long long)(x0 + i) * N + c * NB + r;
+      *o = *o + stage[r * P + pcol(i)];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_fht_b(const float* __restrict__ R,
                                                float* __restrict__ img, Geometry g, int P,
                                                int pair, float scale) {
   extern __shared__ float smem[];
@@ -324,6 +367,7 @@ __global__ void __launch_bounds__(256) k_fht_b(const float* __restrict__ R,
     int l_last = 0, R_last = 0;
     const float* in = A;
     if (g.m > 0) in = run_levels_but_last(A, B, P, NB, g.m, D / kC, &l_last, &R_last);
+    float* stage = (in == A) ? B : A;     // free buffer during the last step
     if (g.m == 0) {
       // NB == 1: the single row is the result (no levels)
       for (int i = threadIdx.x; i < XB; i += blockDim.x) {
@@ -337,9 +381,13 @@ __global__ void __launch_bounds__(256) k_fht_b(const float* __restrict__ R,
         }
       }
     } else if (q == 1) {
-      pass_b_last<true>(R_last, in, P, NBp, l_last, XB, park, nullptr, out, pair, c, NB, x0, scale, N);
+      pass_b_last<true>(R_last, in, P, NBp, l_last, XB, park, nullptr, out, pair, c, NB, x0, scale, N, stage);
     } else {
-      pass_b_last<false>(R_last, in, P, NBp, l_last, XB, nullptr, park, out, pair, c, NB, x0, scale, N);
+      pass_b_last<false>(R_last, in, P, NBp, l_last, XB, nullptr, park, out, pair, c, NB, x0, scale, N, stage);
+      if (pair == 1) {
+        __syncthreads();
+        pass_b_flush_h(stage, P, NB, XB, c, x0, out, N);
+      }
     }
     __syncthreads();
   }
@@ -361,16 +409,17 @@ size_t fht_pass_b_smem(const Geometry& g) {
   return ((size_t)2 * g.NB * pitch_for(g.XB + NBp) + (size_t)g.NB * g.XB) * sizeof(float);
 }
 
-cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, const Geometry& g,
-                              cudaStream_t st, int* launches) {
+cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, int f0, int nf,
+                              long long lin_slice_stride, const Geometry& g, cudaStream_t st,
+                              int* launches) {
   if (slices <= 0) return cudaSuccess;
   const int Hp = (g.H + kC - 1) / kC * kC;
   const int P = pitch_for(g.XA + Hp);
   const size_t smem = fht_pass_a_smem(g);
   cudaError_t e = cudaFuncSetAttribute(k_fht_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.W + g.XA - 1) / g.XA, g.NB, slices * 4);
-  k_fht_a<<<grid, 256, smem, st>>>(lin, R, g, P);
+  dim3 grid((g.W + g.XA - 1) / g.XA, g.NB, slices * nf);
+  k_fht_a<<<grid, 256, smem, st>>>(lin, R, g, P, f0, nf, lin_slice_stride);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -21,14 +21,30 @@ namespace {
 
 __device__ __forceinline__ int pad_idx(int s) { return s + ((s >> 5) << 2); }  // +4 floats per 32
 
-template <int QM>
+template <int QM, int LD = kMaxOrder>
 __device__ __forceinline__ void matvec_acc(const float* M, const float (&v)[QM], float (&acc)[QM]) {
 #pragma unroll
   for (int i = 0; i < QM; ++i) {
     float s = acc[i];
 #pragma unroll
-    for (int j = 0; j < QM; ++j) s = fmaf(M[i * kMaxOrder + j], v[j], s);
+    for (int j = 0; j < QM; ++j) s = fmaf(M[i * LD + j], v[j], s);
     acc[i] = s;
+  }
+}
+
+// Row load/store helpers: all loads of a thread are issued before any use (MLP).
+template <int PER>
+__device__ __forceinline__ void row_to_smem(const float* src, float* row_s, int W, int tid, int nthr) {
+  float4 v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int s = 4 * (tid + k * nthr);
+    if (s < W) v[k] = *reinterpret_cast<const float4*>(src + s);
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int s = 4 * (tid + k * nthr);
+    if (s < W) *reinterpret_cast<float4*>(row_s + pad_idx(s)) = v[k];
   }
 }
 
@@ -40,6 +56,7 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
   extern __shared__ float sm[];
   float* row_s = sm;                                   // W * 36/32 floats (padded)
   float* wagg = sm + (W / 32) * 36 + 64;               // [2][nwarps][QM] warp aggregates
+  float* lm = wagg + 2 * 16 * kMaxOrder;               // [32][QM*QM] A^(L j), compact
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
   const int lane = tid & 31;
@@ -50,13 +67,20 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
   float* dst = out + row * (long long)W;
 
   // ---- coalesced load of the row into padded shared memory ----
-  if (W >= 4) {
-    for (int s = 4 * tid; s < W; s += 4 * nthr) {
-      const float4 v = *reinterpret_cast<const float4*>(src + s);
-      *reinterpret_cast<float4*>(row_s + pad_idx(s)) = v;
-    }
+  // (per thread: W / (4 * nthr) float4, = 8 for every W >= 1024; all in flight)
+  if (W % (4 * nthr) == 0 && W / (4 * nthr) <= 8) {
+    row_to_smem<8>(src, row_s, W, tid, nthr);
+  } else if (W >= 4) {
+    for (int s = 4 * tid; s < W; s += 4 * nthr)
+      *reinterpret_cast<float4*>(row_s + pad_idx(s)) = *reinterpret_cast<const float4*>(src + s);
   } else {
     for (int s = tid; s < W; s += nthr) row_s[pad_idx(s)] = src[s];
+  }
+  if (nwarps > 1) {
+    for (int e = tid; e < 32 * QM * QM; e += nthr) {
+      const int j = e / (QM * QM), r = e % (QM * QM);
+      lm[e] = __ldg(lane_mats + (size_t)j * kMaxOrder * kMaxOrder + (r / QM) * kMaxOrder + (r % QM));
+    }
   }
   __syncthreads();
 
@@ -213,8 +237,8 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
       for (int j = 0; j < QM; ++j) Ka[j] = nk[j];
     }
     // thread carry-in += A^(L*lane) K  (causal),  A^(L*(31-lane)) Ka  (anticausal)
-    matvec_acc<QM>(lane_mats + (size_t)lane * kMaxOrder * kMaxOrder, K, cc);
-    matvec_acc<QM>(lane_mats + (size_t)(31 - lane) * kMaxOrder * kMaxOrder, Ka, ca);
+    matvec_acc<QM, QM>(lm + lane * QM * QM, K, cc);
+    matvec_acc<QM, QM>(lm + (31 - lane) * QM * QM, Ka, ca);
   }
 
   // ---- 3. fix-up with the homogeneous responses, then store ----
@@ -240,7 +264,19 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
     }
   }
   __syncthreads();
-  if (W >= 4) {
+  if (W % (4 * nthr) == 0 && W / (4 * nthr) <= 8) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = 4 * (tid + k * nthr);
+      if (s < W) v[k] = *reinterpret_cast<const float4*>(row_s + pad_idx(s));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = 4 * (tid + k * nthr);
+      if (s < W) *reinterpret_cast<float4*>(dst + s) = v[k];
+    }
+  } else if (W >= 4) {
     for (int s = 4 * tid; s < W; s += 4 * nthr)
       *reinterpret_cast<float4*>(dst + s) = *reinterpret_cast<const float4*>(row_s + pad_idx(s));
   } else {
@@ -253,7 +289,8 @@ static cudaError_t launch_L(const float* in, float* out, long long rows, const G
                             const IirParams& p, const float* lane_mats, cudaStream_t st) {
   const int threads = (g.W >= 32 * L) ? g.W / L : 32;
   const int nwarps = threads / 32;
-  const size_t smem = ((size_t)(g.W / 32 + 1) * 36 + 64 + 2 * nwarps * QM + 16) * sizeof(float);
+  const size_t smem = ((size_t)(g.W / 32 + 1) * 36 + 64 + 2 * 16 * kMaxOrder + 32 * QM * QM + 16) * sizeof(float);
+  (void)nwarps;
   const bool beta = p.beta != 0.0f;
   auto k = beta ? k_iir<QM, L, true> : k_iir<QM, L, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
