@@ -273,6 +273,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   p->max_batch = max_batch;
   const int qm = (std::max(m - 1, q) <= 3) ? 3 : 8;
   p->g = make_geometry(n, qm);
+  p->g.iir_mc = std::max(1, m - 1);
 
   // ---- coefficient tables (double on the host, fp32 for the kernels) ----
   double beta = 0.0;
@@ -320,7 +321,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   grp = std::max<long long>(1, std::min<long long>(grp, max_batch));
   grp = std::min<long long>(grp, 16383);
   p->group = (int)grp;
-  p->per_family = (p->group == 1 && n >= 1024);
+  p->per_family = false;  // measured slower (r01 v2c): launch granularity outweighs L2 reuse
   p->F_bytes = f_slice * p->group;
   p->R_bytes = r_slice * p->group;
   if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess ||

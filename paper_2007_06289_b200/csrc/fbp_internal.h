@@ -40,7 +40,8 @@ struct Geometry {
   int XA;      // pass-A u-tile width
   int XB;      // pass-B x-tile width
   int L;       // IIR per-thread chunk: 32 if W >= 1024, else W/32 (1 if W < 32)
-  int iir_qm;  // compile-time padded order used by the IIR kernel (3 or 8)
+  int iir_qm;  // compile-time padded feedback order of the IIR kernel (3 or 8)
+  int iir_mc;  // number of difference-form feedforward taps c_k (M - 1)
 };
 
 // Kernel launchers (kernels.cu).  All asynchronous on `st`; return the launch error.

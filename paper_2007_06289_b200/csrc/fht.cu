@@ -24,17 +24,32 @@ namespace {
 
 constexpr int kC = 8;  // output columns per register item
 
-__device__ __forceinline__ int pcol(int col) { return col + (col >> 3); }
+// Padded shared-memory tile layout: 4 pad floats after every 32 columns.  Keeps
+// 16-byte alignment of every 4-column group (LDS/STS.128) and makes the
+// stride-8-column lane pattern of the radix items bank-conflict free.
+__device__ __forceinline__ int pc(int col) { return col + ((col >> 5) << 2); }
 
-// Register FHT on 2^R rows: v[b][t], t in [0, kC + 2^R - 1); natural recursion,
-// shifts are compile-time.  Result row r' in v[r'].
+// Register item geometry for radix 2^R: rows NR, halo quads HQ (>= NR-1 columns),
+// window width T = kC + 4*HQ, outputs at window offset O = 4*HQ.
 template <int R>
-__device__ __forceinline__ void local_fht(float (&v)[1 << R][kC + (1 << R) - 1]) {
-  constexpr int NR = 1 << R;
-  constexpr int T = kC + NR - 1;
+struct RT {
+  static constexpr int NR = 1 << R;
+  static constexpr int HQ = (NR - 1 + 3) / 4;
+  static constexpr int O = 4 * HQ;
+  static constexpr int T = kC + O;
+};
+
+// Register FHT on 2^R rows (natural recursion, compile-time shifts), computing at
+// each level only the columns the final outputs [O, T) depend on.
+template <int R>
+__device__ __forceinline__ void local_fht(float (&v)[RT<R>::NR][RT<R>::T]) {
+  constexpr int NR = RT<R>::NR;
+  constexpr int T = RT<R>::T;
+  // lower column bound needed at the output of level lvl: O - sum_{k>lvl} 2^k
 #pragma unroll
   for (int lvl = 0; lvl < R; ++lvl) {
     const int h = 1 << lvl;
+    const int lb = RT<R>::O - ((1 << R) - (1 << (lvl + 1)));
     float w[NR][T];
 #pragma unroll
     for (int y = 0; y < NR; ++y) {
@@ -44,35 +59,71 @@ __device__ __forceinline__ void local_fht(float (&v)[1 << R][kC + (1 << R) - 1])
       const int sh = (yp + 1) >> 1;
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        const float bv = (t >= sh) ? v[blk + h + lo][t - sh] : 0.0f;
-        w[y][t] = v[blk + lo][t] + bv;
+        if (t >= lb) {
+          const float bv = (t >= sh) ? v[blk + h + lo][t - sh] : 0.0f;
+          w[y][t] = v[blk + lo][t] + bv;
+        }
       }
     }
 #pragma unroll
     for (int y = 0; y < NR; ++y)
 #pragma unroll
-      for (int t = 0; t < T; ++t) v[y][t] = w[y][t];
+      for (int t = 0; t < T; ++t)
+        if (t >= lb) v[y][t] = w[y][t];
   }
 }
 
-// Load the 2^R pre-shifted input rows of item (G, c, chunk j) from a padded tile.
-// Column col_lo = j*kC - (2^R - 1); input row b' read at col - c*b'.
+// Load the window [col0 - O, col0 - O + T) of the 2^R pre-shifted input rows of
+// item (G, c, chunk at col0): row b' read at virtual column col - c*b'.
 template <int R>
 __device__ __forceinline__ void load_item(const float* tile, int P, int l, int G, int c, int col0,
-                                          float (&v)[1 << R][kC + (1 << R) - 1]) {
-  constexpr int NR = 1 << R;
-  constexpr int T = kC + NR - 1;
+                                          float (&v)[RT<R>::NR][RT<R>::T]) {
+  constexpr int NR = RT<R>::NR;
+  constexpr int T = RT<R>::T;
 #pragma unroll
   for (int b = 0; b < NR; ++b) {
     const int row = ((G << R) + b) * (1 << l) + c;
     const float* rp = tile + (size_t)row * P;
-    const int cs = col0 - (NR - 1) - c * b;
+    const int cs = col0 - RT<R>::O - c * b;
+    if (cs >= 0) {
+      const int ws = cs & ~3;
+      const int o = cs & 3;
+      float w[T + 4];
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int col = cs + t;
-      v[b][t] = (col >= 0) ? rp[pcol(col)] : 0.0f;
+      for (int q = 0; q < T / 4 + 1; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(rp + pc(ws + 4 * q));
+        w[4 * q] = f.x;
+        w[4 * q + 1] = f.y;
+        w[4 * q + 2] = f.z;
+        w[4 * q + 3] = f.w;
+      }
+      if (o == 0) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) v[b][t] = w[t];
+      } else if (o == 1) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) v[b][t] = w[t + 1];
+      } else if (o == 2) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) v[b][t] = w[t + 2];
+      } else {
+#pragma unroll
+        for (int t = 0; t < T; ++t) v[b][t] = w[t + 3];
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int col = cs + t;
+        v[b][t] = (col >= 0) ? rp[pc(col)] : 0.0f;
+      }
     }
   }
+}
+
+// Store 8 outputs at columns [col0, col0 + 8) of a padded row (2 x STS.128).
+__device__ __forceinline__ void store8(float* rp, int col0, const float* s) {
+  *reinterpret_cast<float4*>(rp + pc(col0)) = make_float4(s[0], s[1], s[2], s[3]);
+  *reinterpret_cast<float4*>(rp + pc(col0 + 4)) = make_float4(s[4], s[5], s[6], s[7]);
 }
 
 // One radix step in shared memory: tiles in -> out (padded, pitch P), items over
@@ -89,15 +140,12 @@ __device__ void radix_step_smem(const float* in, float* out, int P, int rows, in
     const int gc = it / nchunks;
     const int c = gc % nch;
     const int G = gc / nch;
-    float v[NR][kC + NR - 1];
+    float v[NR][RT<R>::T];
     load_item<R>(in, P, l, G, c, j * kC, v);
     local_fht<R>(v);
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      float* op = out + (size_t)((G << (l + R)) + c * NR + r) * P;
-#pragma unroll
-      for (int t = 0; t < kC; ++t) op[pcol(j * kC + t)] = v[r][NR - 1 + t];
-    }
+    for (int r = 0; r < NR; ++r)
+      store8(out + (size_t)((G << (l + R)) + c * NR + r) * P, j * kC, &v[r][RT<R>::O]);
   }
 }
 
@@ -156,7 +204,7 @@ __device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp,
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int j = chunk0 + it % nchunks;
     const int c = it / nchunks;
-    float v[NR][kC + NR - 1];
+    float v[NR][RT<R>::T];
     load_item<R>(in, P, l, 0, c, j * kC, v);
     local_fht<R>(v);
     const int ubase = u0 - Hp + j * kC;
@@ -168,12 +216,12 @@ __device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp,
       float* out = dstR + (long long)cf * g.WR + (cf * b - g.N + g.NB);
       if (ubase >= ulo && ubase + kC <= uhi) {
 #pragma unroll
-        for (int t = 0; t < kC; ++t) out[ubase + t] = v[r][NR - 1 + t];
+        for (int t = 0; t < kC; ++t) out[ubase + t] = v[r][RT<R>::O + t];
       } else {
 #pragma unroll
         for (int t = 0; t < kC; ++t) {
           const int u = ubase + t;
-          if (u >= ulo && u < uhi) out[u] = v[r][NR - 1 + t];
+          if (u >= ulo && u < uhi) out[u] = v[r][RT<R>::O + t];
         }
       }
     }
@@ -214,11 +262,7 @@ __device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, c
       if (e < total) {
         const int r = e / q4;
         const int c4 = (e - r * q4) * 4;
-        float* d = tile + (size_t)r * P + pcol(c4);
-        d[0] = v[k].x;
-        d[1] = v[k].y;
-        d[2] = v[k].z;
-        d[3] = v[k].w;
+        *reinterpret_cast<float4*>(tile + (size_t)r * P + pc(c4)) = v[k];
       }
     }
   }
@@ -268,7 +312,7 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int jj = it % nchunks;
     const int cc = it / nchunks;
-    float v[NR][kC + NR - 1];
+    float v[NR][RT<R>::T];
     load_item<R>(in, P, l, 0, cc, NBp + jj * kC, v);
     local_fht<R>(v);
 #pragma unroll
@@ -276,13 +320,13 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
       const int rf = cc * NR + r;               // final row within the channel block
       if (PARK) {
 #pragma unroll
-        for (int t = 0; t < kC; ++t) park[rf * XB + jj * kC + t] = v[r][NR - 1 + t];
+        for (int t = 0; t < kC; ++t) park[rf * XB + jj * kC + t] = v[r][RT<R>::O + t];
       } else {
         float s[kC];
 #pragma unroll
         for (int t = 0; t < kC; ++t) {
           const int i = jj * kC + t;
-          s[t] = scale * (v[r][NR - 1 + t] + parked[rf * XB + (XB - 1 - i)]);
+          s[t] = scale * (v[r][RT<R>::O + t] + parked[rf * XB + (XB - 1 - i)]);
         }
         const int y = c * NB + rf;
         const int xb = x0 + jj * kC;
@@ -300,7 +344,7 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
           // transposed pair: park in the free tile buffer (padded rows), written
           // out coalesced by pass_b_flush_h after the barrier
 #pragma unroll
-          for (int t = 0; t < kC; ++t) stage[rf * P + pcol(jj * kC + t)] = s[t];
+          store8(stage + (size_t)rf * P, jj * kC, s);
         }
       }
     }
@@ -327,10 +371,10 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
       if (x0 + i >= N) continue;
       float4* o = reinterpret_cast<float4*>(out + (long long)(x0 + i) * N + c * NB + r);
       float4 v = *o;
-      v.x += stage[(r + 0) * P + pcol(i)];
-      v.y += stage[(r + 1) * P + pcol(i)];
-      v.z += stage[(r + 2) * P + pcol(i)];
-      v.w += stage[(r + 3) * P + pcol(i)];
+      v.x += stage[(r + 0) * P + pc(i)];
+      v.y += stage[(r + 1) * P + pc(i)];
+      v.z += stage[(r + 2) * P + pc(i)];
+      v.w += stage[(r + 3) * P + pc(i)];
       *o = v;
     }
   } else {
@@ -339,7 +383,7 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
       const int r = e - i * NB;
       if (x0 + i >= N) continue;
       float* o = out + (long long)(x0 + i) * N + c * NB + r;
-      *o = *o + stage[r * P + pcol(i)];
+      *o = *o + stage[r * P + pc(i)];
     }
   }
 }
@@ -371,7 +415,7 @@ __global__ void __launch_bounds__(256, 2) k_fht_b(const float* __restrict__ R,
     if (g.m == 0) {
       // NB == 1: the single row is the result (no levels)
       for (int i = threadIdx.x; i < XB; i += blockDim.x) {
-        const float v = in[pcol(NBp + i)];
+        const float v = in[pc(NBp + i)];
         if (q == 1) {
           park[i] = v;
         } else if (x0 + i < N) {
@@ -394,9 +438,9 @@ __global__ void __launch_bounds__(256, 2) k_fht_b(const float* __restrict__ R,
 }
 
 static int pitch_for(int D) {
-  int P = D + (D >> 3) + 1;
-  if ((P & 1) == 0) ++P;
-  return P;
+  // covers the widest window read (D + 8 columns) in the padded layout, mult. of 4
+  const int w = D + 8;
+  return (w + ((w >> 5) << 2) + 4 + 3) & ~3;
 }
 
 size_t fht_pass_a_smem(const Geometry& g) {

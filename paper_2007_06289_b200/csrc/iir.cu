@@ -50,7 +50,7 @@ __device__ __forceinline__ void row_to_smem(const float* src, float* row_s, int 
 
 }  // namespace
 
-template <int QM, int L, bool BETA>
+template <int QM, int MC, int L, bool BETA>
 __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
                                              const float* __restrict__ lane_mats, IirParams p) {
   extern __shared__ float sm[];
@@ -110,69 +110,56 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
     for (int i = 0; i < L; ++i) x[i] = active ? row_s[pad_idx(start + i)] : 0.0f;
   }
 
-  // ---- 1a. causal zero-state sweep:  u = beta x + sum_k c_k D[n-k], D[n] = x[n]-x[n-1] ----
-  float vc[QM];
+  // ---- 1. both zero-state sweeps at once, packed in f32x2 (FFMA2/FADD2):
+  //   lane .x runs the causal recursion at sample k (left to right),
+  //   lane .y the anticausal one at sample L-1-k (right to left).
+  //   causal:     u = beta x[n] + sum_k c_k D[n-k],  D[n] = x[n] - x[n-1]
+  //   anticausal: u = beta x[n] + sum_k c_k E[n+k],  E[n] = x[n] - x[n+1]
+  //   y = u - sum_k a_k y[n -/+ k]                        (Eq.13, both signs)
+  float vc[QM], va[QM];
   {
-    float dh[QM];
+    float2 dh[MC > 1 ? MC - 1 : 1];      // (D[n-1-k], E[n+1+k])
 #pragma unroll
-    for (int k = 0; k < QM; ++k) dh[k] = xl[k] - xl[k + 1];
-    float yq[QM];
+    for (int k = 0; k < MC - 1; ++k) dh[k] = make_float2(xl[k] - xl[k + 1], xr[k] - xr[k + 1]);
+    float2 yq[QM];
 #pragma unroll
-    for (int k = 0; k < QM; ++k) yq[k] = 0.0f;
-    float xprev = xl[0];
+    for (int k = 0; k < QM; ++k) yq[k] = make_float2(0.0f, 0.0f);
+    float2 xprev = make_float2(xl[0], xr[0]);
+    const float2 m1 = make_float2(-1.0f, -1.0f);
+    float2 na[QM], cp[MC];
+#pragma unroll
+    for (int k = 0; k < QM; ++k) na[k] = make_float2(-p.a[k], -p.a[k]);
+#pragma unroll
+    for (int k = 0; k < MC; ++k) cp[k] = make_float2(p.c[k], p.c[k]);
+    const float2 bp = make_float2(p.beta, p.beta);
+    float2 yp[L];
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      const float d = x[i] - xprev;
-      xprev = x[i];
-      float u = BETA ? p.beta * x[i] : 0.0f;
-      u = fmaf(p.c[0], d, u);
+      const float2 xx = make_float2(x[i], x[L - 1 - i]);
+      const float2 d = __ffma2_rn(m1, xprev, xx);          // (D[n], E[n'])
+      xprev = xx;
+      float2 u = BETA ? __fmul2_rn(bp, xx) : make_float2(0.0f, 0.0f);
+      u = BETA ? __ffma2_rn(cp[0], d, u) : __fmul2_rn(cp[0], d);
 #pragma unroll
-      for (int k = 1; k < QM; ++k) u = fmaf(p.c[k], dh[k - 1], u);
+      for (int k = 1; k < MC; ++k) u = __ffma2_rn(cp[k], dh[k - 1], u);
 #pragma unroll
-      for (int k = QM - 1; k > 0; --k) dh[k] = dh[k - 1];
-      dh[0] = d;
-      float v = u;
+      for (int k = MC - 2; k > 0; --k) dh[k] = dh[k - 1];
+      if (MC > 1) dh[0] = d;
+      float2 v = u;
 #pragma unroll
-      for (int k = QM - 1; k >= 0; --k) v = fmaf(-p.a[k], yq[k], v);
-#pragma unroll
-      for (int k = QM - 1; k > 0; --k) yq[k] = yq[k - 1];
-      yq[0] = v;
-      y[i] = v;
-    }
-#pragma unroll
-    for (int k = 0; k < QM; ++k) vc[k] = active ? yq[k] : 0.0f;
-  }
-  // ---- 1b. anticausal zero-state sweep:  u = beta x + sum_k c_k E[n+k], E[n] = x[n]-x[n+1] ----
-  float va[QM];
-  {
-    float eh[QM];
-#pragma unroll
-    for (int k = 0; k < QM; ++k) eh[k] = xr[k] - xr[k + 1];
-    float yq[QM];
-#pragma unroll
-    for (int k = 0; k < QM; ++k) yq[k] = 0.0f;
-    float xnext = xr[0];
-#pragma unroll
-    for (int i = L - 1; i >= 0; --i) {
-      const float e = x[i] - xnext;
-      xnext = x[i];
-      float u = BETA ? p.beta * x[i] : 0.0f;
-      u = fmaf(p.c[0], e, u);
-#pragma unroll
-      for (int k = 1; k < QM; ++k) u = fmaf(p.c[k], eh[k - 1], u);
-#pragma unroll
-      for (int k = QM - 1; k > 0; --k) eh[k] = eh[k - 1];
-      eh[0] = e;
-      float v = u;
-#pragma unroll
-      for (int k = QM - 1; k >= 0; --k) v = fmaf(-p.a[k], yq[k], v);
+      for (int k = QM - 1; k >= 0; --k) v = __ffma2_rn(na[k], yq[k], v);
 #pragma unroll
       for (int k = QM - 1; k > 0; --k) yq[k] = yq[k - 1];
       yq[0] = v;
-      y[i] += v;
+      yp[i] = v;
     }
 #pragma unroll
-    for (int k = 0; k < QM; ++k) va[k] = active ? yq[k] : 0.0f;
+    for (int i = 0; i < L; ++i) y[i] = yp[i].x + yp[L - 1 - i].y;
+#pragma unroll
+    for (int k = 0; k < QM; ++k) {
+      vc[k] = active ? yq[k].x : 0.0f;
+      va[k] = active ? yq[k].y : 0.0f;
+    }
   }
 
   // ---- 2. scans of the chunk states across threads ----
@@ -284,7 +271,7 @@ __global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
   }
 }
 
-template <int QM, int L>
+template <int QM, int MC, int L>
 static cudaError_t launch_L(const float* in, float* out, long long rows, const Geometry& g,
                             const IirParams& p, const float* lane_mats, cudaStream_t st) {
   const int threads = (g.W >= 32 * L) ? g.W / L : 32;
@@ -292,7 +279,7 @@ static cudaError_t launch_L(const float* in, float* out, long long rows, const G
   const size_t smem = ((size_t)(g.W / 32 + 1) * 36 + 64 + 2 * 16 * kMaxOrder + 32 * QM * QM + 16) * sizeof(float);
   (void)nwarps;
   const bool beta = p.beta != 0.0f;
-  auto k = beta ? k_iir<QM, L, true> : k_iir<QM, L, false>;
+  auto k = beta ? k_iir<QM, MC, L, true> : k_iir<QM, MC, L, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   for (long long r0 = 0; r0 < rows; r0 += 2147483647LL) {
@@ -302,16 +289,16 @@ static cudaError_t launch_L(const float* in, float* out, long long rows, const G
   return cudaGetLastError();
 }
 
-template <int QM>
+template <int QM, int MC>
 static cudaError_t launch_qm(const float* in, float* out, long long rows, const Geometry& g,
                              const IirParams& p, const float* lane_mats, cudaStream_t st) {
   switch (g.L) {
-    case 1: return launch_L<QM, 1>(in, out, rows, g, p, lane_mats, st);
-    case 2: return launch_L<QM, 2>(in, out, rows, g, p, lane_mats, st);
-    case 4: return launch_L<QM, 4>(in, out, rows, g, p, lane_mats, st);
-    case 8: return launch_L<QM, 8>(in, out, rows, g, p, lane_mats, st);
-    case 16: return launch_L<QM, 16>(in, out, rows, g, p, lane_mats, st);
-    default: return launch_L<QM, 32>(in, out, rows, g, p, lane_mats, st);
+    case 1: return launch_L<QM, MC, 1>(in, out, rows, g, p, lane_mats, st);
+    case 2: return launch_L<QM, MC, 2>(in, out, rows, g, p, lane_mats, st);
+    case 4: return launch_L<QM, MC, 4>(in, out, rows, g, p, lane_mats, st);
+    case 8: return launch_L<QM, MC, 8>(in, out, rows, g, p, lane_mats, st);
+    case 16: return launch_L<QM, MC, 16>(in, out, rows, g, p, lane_mats, st);
+    default: return launch_L<QM, MC, 32>(in, out, rows, g, p, lane_mats, st);
   }
 }
 
@@ -319,8 +306,10 @@ cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const G
                             const IirParams& p, const float* lane_mats, cudaStream_t st,
                             int* launches) {
   if (rows <= 0) return cudaSuccess;
-  cudaError_t e = (g.iir_qm == 3) ? launch_qm<3>(in, out, rows, g, p, lane_mats, st)
-                                  : launch_qm<8>(in, out, rows, g, p, lane_mats, st);
+  // M-1 <= 2 difference taps and Q <= 3 (the paper's M = Q = 3) get the short
+  // specialisation; everything else the general order-8 one (zero-padded).
+  cudaError_t e = (g.iir_qm == 3 && g.iir_mc <= 2) ? launch_qm<3, 2>(in, out, rows, g, p, lane_mats, st)
+                                                  : launch_qm<8, 8>(in, out, rows, g, p, lane_mats, st);
   if (launches) ++*launches;
   return e;
 }
