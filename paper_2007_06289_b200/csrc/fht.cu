@@ -29,6 +29,16 @@ constexpr int kC = 8;  // output columns per register item
 // stride-8-column lane pattern of the radix items bank-conflict free.
 __device__ __forceinline__ int pc(int col) { return col + ((col >> 5) << 2); }
 
+// Division by a runtime divisor d (< 2^16) of n (< 2^16) without the integer
+// divide sequence: n / d = umulhi(n, ceil(2^32 / d)).
+struct FastDiv {
+  unsigned m;
+  int d;
+  __device__ __forceinline__ explicit FastDiv(int dd)
+      : m((unsigned)((0x100000000ULL + (unsigned)dd - 1) / (unsigned)dd)), d(dd) {}
+  __device__ __forceinline__ int div(int n) const { return (int)__umulhi((unsigned)n, m); }
+};
+
 // Register item geometry for radix 2^R: rows NR, halo quads HQ (>= NR-1 columns),
 // window width T = kC + 4*HQ, outputs at window offset O = 4*HQ.
 template <int R>
@@ -135,11 +145,12 @@ __device__ void radix_step_smem(const float* in, float* out, int P, int rows, in
   const int nch = 1 << l;                  // channels
   const int ngroups = rows >> (l + R);
   const int items = ngroups * nch * nchunks;
+  const FastDiv fd(nchunks);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int j = chunk0 + it % nchunks;
-    const int gc = it / nchunks;
-    const int c = gc % nch;
-    const int G = gc / nch;
+    const int gc = fd.div(it);
+    const int j = chunk0 + it - gc * nchunks;
+    const int c = gc & (nch - 1);
+    const int G = gc >> l;
     float v[NR][RT<R>::T];
     load_item<R>(in, P, l, G, c, j * kC, v);
     local_fht<R>(v);
@@ -201,9 +212,10 @@ __device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp,
   const int nchunks = XA / kC;
   const int chunk0 = Hp / kC;
   const int items = nch * nchunks;   // a single group in the last step
+  const FastDiv fd(nchunks);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int j = chunk0 + it % nchunks;
-    const int c = it / nchunks;
+    const int c = fd.div(it);
+    const int j = chunk0 + it - c * nchunks;
     float v[NR][RT<R>::T];
     load_item<R>(in, P, l, 0, c, j * kC, v);
     local_fht<R>(v);
@@ -237,13 +249,14 @@ __device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, c
   const int q4 = D >> 2;
   const int total = rows * q4;
   const bool vec = ((g0 & 3) == 0) && ((gp & 3) == 0);
+  const FastDiv fq(q4);
   for (int e0 = threadIdx.x; e0 < total; e0 += kU * blockDim.x) {
     float4 v[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
       const int e = e0 + k * blockDim.x;
       if (e < total) {
-        const int r = e / q4;
+        const int r = fq.div(e);
         const int u = g0 + (e - r * q4) * 4;
         const float* rp = src + (long long)r * gp;
         if (vec && u >= 0 && u + 3 < gw) {
@@ -260,7 +273,7 @@ __device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, c
     for (int k = 0; k < kU; ++k) {
       const int e = e0 + k * blockDim.x;
       if (e < total) {
-        const int r = e / q4;
+        const int r = fq.div(e);
         const int c4 = (e - r * q4) * 4;
         *reinterpret_cast<float4*>(tile + (size_t)r * P + pc(c4)) = v[k];
       }
@@ -309,9 +322,10 @@ __device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp
   const int nch = 1 << l;
   const int nchunks = XB / kC;
   const int items = nch * nchunks;
+  const FastDiv fd(nchunks);
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int jj = it % nchunks;
-    const int cc = it / nchunks;
+    const int cc = fd.div(it);
+    const int jj = it - cc * nchunks;
     float v[NR][RT<R>::T];
     load_item<R>(in, P, l, 0, cc, NBp + jj * kC, v);
     local_fht<R>(v);
@@ -365,8 +379,9 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
                                                int x0, float* out, int N) {
   if ((NB & 3) == 0) {
     const int q = NB >> 2;
+    const FastDiv fq(q);
     for (int e = threadIdx.x; e < XB * q; e += blockDim.x) {
-      const int i = e / q;
+      const int i = fq.div(e);
       const int r = (e - i * q) * 4;
       if (x0 + i >= N) continue;
       float4* o = reinterpret_cast<float4*>(out + (long long)(x0 + i) * N + c * NB + r);
@@ -378,8 +393,9 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
       *o = v;
     }
   } else {
+    const FastDiv fn(NB);
     for (int e = threadIdx.x; e < XB * NB; e += blockDim.x) {
-      const int i = e / NB;
+      const int i = fn.div(e);
       const int r = e - i * NB;
       if (x0 + i >= N) continue;
       float* o = out + (long long)(x0 + i) * N + c * NB + r;
@@ -438,9 +454,10 @@ __global__ void __launch_bounds__(256, 2) k_fht_b(const float* __restrict__ R,
 }
 
 static int pitch_for(int D) {
-  // covers the widest window read (D + 8 columns) in the padded layout, mult. of 4
-  const int w = D + 8;
-  return (w + ((w >> 5) << 2) + 4 + 3) & ~3;
+  // widest column read by an item window is D + 3 (see load_item); padded layout,
+  // rounded to a multiple of 4 floats (16-byte rows)
+  const int w = D + 4;
+  return (w + ((w >> 5) << 2) + 3) & ~3;
 }
 
 size_t fht_pass_a_smem(const Geometry& g) {
