@@ -6,38 +6,89 @@
 // levels combine 2^R consecutive blocks; by d_y(t) = c*b' + d^(R)_{r'}(b') + ... :
 //   out[G*2^(l+R) + c*2^R + r'][u] = sum_{b'<2^R} in[(G*2^R + b')*2^l + c][u - c*b' - d^(R)_{r'}(b')]
 // i.e. a pre-shift c*b' of each input row (addressing only) followed by an R-level
-// FHT with compile-time shifts, done in registers on 2^R rows x 8 columns
-// (+ 2^R - 1 halo columns).  Shared-memory tiles use a padded layout
-// (col + col/8) so that lanes working on consecutive 8-column chunks are
-// bank-conflict free.
+// FHT with compile-time shifts, done in registers on 2^R rows x 8 columns (+ halo).
 //
 //   pass A (k_fht_a): k1 levels on each block of H = 2^k1 rows of the filtered
-//     linogram, tile = H rows x (XA core + H halo) columns; output stored compactly
-//     and only where pass B reads it (u in [N - b(c+1), 2N - c b)).
-//   pass B (k_fht_b): per channel c, rows b of G_c[b][v] = R_A[b][c][v - c b],
-//     m levels, then the family pair of Eq.22 (mirror) and the weight.
+//     linogram; tile = H rows x (Hp halo + XA core) columns.  Output stored
+//     compactly, only where pass B reads it (u in [N - b(c+1), 2N - c b)).
+//   pass B (k_fht_b): per channel c, rows b of G_c[b][v] = R_A[b][c][v - c b]
+//     (the compact layout already applies the pre-shift), m levels, then the family
+//     pair of Eq.22 (mirror), the weight, and the store.
+// Both kernels are persistent (grid = resident CTAs) and prefetch the next tile
+// with cp.async while computing the current one.
 #include "fbp_internal.h"
+
+#include <algorithm>
 
 namespace fbp {
 
 namespace {
 
-constexpr int kC = 8;  // output columns per register item
+constexpr int kC = 8;        // output columns per register item
+constexpr int kThreads = 256;
 
 // Padded shared-memory tile layout: 4 pad floats after every 32 columns.  Keeps
-// 16-byte alignment of every 4-column group (LDS/STS.128) and makes the
-// stride-8-column lane pattern of the radix items bank-conflict free.
+// 16-byte alignment of every 4-column group (cp.async / LDS / STS .128) and makes
+// the stride-8-column lane pattern of the radix items bank-conflict free.
 __device__ __forceinline__ int pc(int col) { return col + ((col >> 5) << 2); }
 
 // Division by a runtime divisor d (< 2^16) of n (< 2^16) without the integer
-// divide sequence: n / d = umulhi(n, ceil(2^32 / d)).
+// divide sequence: n / d = umulhi(n, ceil(2^32 / d)); d = 1 handled separately.
 struct FastDiv {
   unsigned m;
   int d;
   __device__ __forceinline__ explicit FastDiv(int dd)
-      : m((unsigned)((0x100000000ULL + (unsigned)dd - 1) / (unsigned)dd)), d(dd) {}
-  __device__ __forceinline__ int div(int n) const { return (int)__umulhi((unsigned)n, m); }
+      : m(dd > 1 ? (unsigned)((0x100000000ULL + (unsigned)dd - 1) / (unsigned)dd) : 0u), d(dd) {}
+  __device__ __forceinline__ int div(int n) const {
+    return d > 1 ? (int)__umulhi((unsigned)n, m) : n;
+  }
 };
+
+// ---- cp.async (zero-fill when !valid) ----
+__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gsrc),
+               "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT));
+}
+
+// Asynchronously fill a `rows` x D padded tile (pitch P) from global rows of
+// pitch gp, starting at global column g0 (may be negative); columns outside
+// [0, gw) are zero-filled.  Rows are spread over warps, 4-column groups over lanes.
+// Commits one cp.async group.
+__device__ __forceinline__ void fill_async(float* tile, int P, int rows, int D, const float* src,
+                                           long long gp, int g0, int gw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q4 = D >> 2;
+  const bool vec = ((g0 & 3) == 0) && ((gp & 3) == 0) && ((gw & 3) == 0);
+  for (int r = warp; r < rows; r += kThreads / 32) {
+    const float* rp = src + (long long)r * gp;
+    float* tp = tile + (size_t)r * P;
+    for (int q = lane; q < q4; q += 32) {
+      const int u = g0 + 4 * q;
+      if (vec) {
+        const bool ok = (u >= 0) && (u < gw);
+        cp_async16(tp + pc(4 * q), ok ? rp + u : rp, ok);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const bool ok = (u + e >= 0) && (u + e < gw);
+          cp_async4(tp + pc(4 * q + e), ok ? rp + u + e : rp, ok);
+        }
+      }
+    }
+  }
+  cp_async_commit();
+}
 
 // Register item geometry for radix 2^R: rows NR, halo quads HQ (>= NR-1 columns),
 // window width T = kC + 4*HQ, outputs at window offset O = 4*HQ.
@@ -55,7 +106,6 @@ template <int R>
 __device__ __forceinline__ void local_fht(float (&v)[RT<R>::NR][RT<R>::T]) {
   constexpr int NR = RT<R>::NR;
   constexpr int T = RT<R>::T;
-  // lower column bound needed at the output of level lvl: O - sum_{k>lvl} 2^k
 #pragma unroll
   for (int lvl = 0; lvl < R; ++lvl) {
     const int h = 1 << lvl;
@@ -84,42 +134,36 @@ __device__ __forceinline__ void local_fht(float (&v)[RT<R>::NR][RT<R>::T]) {
 }
 
 // Load the window [col0 - O, col0 - O + T) of the 2^R pre-shifted input rows of
-// item (G, c, chunk at col0): row b' read at virtual column col - c*b'.
-template <int R>
+// item (G, c, chunk at col0): row b read at virtual column col - c*b.  CM = c & 3
+// makes every row's alignment offset (-c*b) & 3 a compile-time constant, so the
+// aligned LDS.128 quads land directly in the item registers (no moves).
+template <int R, int CM>
 __device__ __forceinline__ void load_item(const float* tile, int P, int l, int G, int c, int col0,
                                           float (&v)[RT<R>::NR][RT<R>::T]) {
   constexpr int NR = RT<R>::NR;
   constexpr int T = RT<R>::T;
 #pragma unroll
   for (int b = 0; b < NR; ++b) {
+    const int o = (4 - ((CM * b) & 3)) & 3;             // (-c*b) & 3, compile-time
     const int row = ((G << R) + b) * (1 << l) + c;
     const float* rp = tile + (size_t)row * P;
-    const int cs = col0 - RT<R>::O - c * b;
+    const int cs = col0 - RT<R>::O - c * b;              // first window column
     if (cs >= 0) {
-      const int ws = cs & ~3;
-      const int o = cs & 3;
-      float w[T + 4];
+      const int ws = cs - o;                             // 4-aligned
+      constexpr int NQ = (T + 3 + 3) / 4;                // enough quads for any o
+      float w[NQ * 4];
 #pragma unroll
-      for (int q = 0; q < T / 4 + 1; ++q) {
-        const float4 f = *reinterpret_cast<const float4*>(rp + pc(ws + 4 * q));
-        w[4 * q] = f.x;
-        w[4 * q + 1] = f.y;
-        w[4 * q + 2] = f.z;
-        w[4 * q + 3] = f.w;
+      for (int q = 0; q < NQ; ++q) {
+        if (4 * q < T + o) {
+          const float4 f = *reinterpret_cast<const float4*>(rp + pc(ws + 4 * q));
+          w[4 * q] = f.x;
+          w[4 * q + 1] = f.y;
+          w[4 * q + 2] = f.z;
+          w[4 * q + 3] = f.w;
+        }
       }
-      if (o == 0) {
 #pragma unroll
-        for (int t = 0; t < T; ++t) v[b][t] = w[t];
-      } else if (o == 1) {
-#pragma unroll
-        for (int t = 0; t < T; ++t) v[b][t] = w[t + 1];
-      } else if (o == 2) {
-#pragma unroll
-        for (int t = 0; t < T; ++t) v[b][t] = w[t + 2];
-      } else {
-#pragma unroll
-        for (int t = 0; t < T; ++t) v[b][t] = w[t + 3];
-      }
+      for (int t = 0; t < T; ++t) v[b][t] = w[t + o];
     } else {
 #pragma unroll
       for (int t = 0; t < T; ++t) {
@@ -130,62 +174,79 @@ __device__ __forceinline__ void load_item(const float* tile, int P, int l, int G
   }
 }
 
+// Process one item: load (alignment specialised on c & 3), R register levels,
+// then the epilogue epi(v) with outputs v[r][O + t], t < 8.
+template <int R, int CM, typename Epi>
+__device__ __forceinline__ void item_cm(const float* tile, int P, int l, int G, int c, int col0,
+                                        Epi& epi) {
+  float v[RT<R>::NR][RT<R>::T];
+  load_item<R, CM>(tile, P, l, G, c, col0, v);
+  local_fht<R>(v);
+  epi(v);
+}
+template <int R, typename Epi>
+__device__ __forceinline__ void item(const float* tile, int P, int l, int G, int c, int col0,
+                                     Epi& epi) {
+  switch (c & 3) {
+    case 0: item_cm<R, 0>(tile, P, l, G, c, col0, epi); break;
+    case 1: item_cm<R, 1>(tile, P, l, G, c, col0, epi); break;
+    case 2: item_cm<R, 2>(tile, P, l, G, c, col0, epi); break;
+    default: item_cm<R, 3>(tile, P, l, G, c, col0, epi); break;
+  }
+}
+
 // Store 8 outputs at columns [col0, col0 + 8) of a padded row (2 x STS.128).
 __device__ __forceinline__ void store8(float* rp, int col0, const float* s) {
   *reinterpret_cast<float4*>(rp + pc(col0)) = make_float4(s[0], s[1], s[2], s[3]);
   *reinterpret_cast<float4*>(rp + pc(col0 + 4)) = make_float4(s[4], s[5], s[6], s[7]);
 }
 
-// One radix step in shared memory: tiles in -> out (padded, pitch P), items over
-// output chunks [chunk0, chunk0 + nchunks).
+// One intermediate radix step in shared memory: in -> out (padded, pitch P).
 template <int R>
-__device__ void radix_step_smem(const float* in, float* out, int P, int rows, int l, int chunk0,
-                                int nchunks) {
+__device__ void radix_step_smem(const float* in, float* out, int P, int rows, int l, int nchunks) {
   constexpr int NR = 1 << R;
-  const int nch = 1 << l;                  // channels
-  const int ngroups = rows >> (l + R);
-  const int items = ngroups * nch * nchunks;
+  const int nch = 1 << l;
+  const int items = (rows >> (l + R)) * nch * nchunks;
   const FastDiv fd(nchunks);
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  for (int it = threadIdx.x; it < items; it += kThreads) {
     const int gc = fd.div(it);
-    const int j = chunk0 + it - gc * nchunks;
+    const int j = it - gc * nchunks;
     const int c = gc & (nch - 1);
     const int G = gc >> l;
-    float v[NR][RT<R>::T];
-    load_item<R>(in, P, l, G, c, j * kC, v);
-    local_fht<R>(v);
+    auto epi = [&](float (&v)[NR][RT<R>::T]) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r)
-      store8(out + (size_t)((G << (l + R)) + c * NR + r) * P, j * kC, &v[r][RT<R>::O]);
+      for (int r = 0; r < NR; ++r)
+        store8(out + (size_t)((G << (l + R)) + c * NR + r) * P, j * kC, &v[r][RT<R>::O]);
+    };
+    item<R>(in, P, l, G, c, j * kC, epi);
   }
 }
 
 __device__ __forceinline__ void radix_step_dispatch(int R, const float* in, float* out, int P,
-                                                    int rows, int l, int chunk0, int nchunks) {
-  if (R == 3) radix_step_smem<3>(in, out, P, rows, l, chunk0, nchunks);
-  else if (R == 2) radix_step_smem<2>(in, out, P, rows, l, chunk0, nchunks);
-  else radix_step_smem<1>(in, out, P, rows, l, chunk0, nchunks);
+                                                    int rows, int l, int nchunks) {
+  if (R == 3) radix_step_smem<3>(in, out, P, rows, l, nchunks);
+  else if (R == 2) radix_step_smem<2>(in, out, P, rows, l, nchunks);
+  else radix_step_smem<1>(in, out, P, rows, l, nchunks);
 }
 
-// Split `levels` into radix steps of at most 3 levels: returns the radix of step s.
+// Split `levels` into radix steps of at most 3 levels: radix of step s.
+// 1->[1] 2->[2] 3->[3] 4->[2,2] 5->[3,2] 6->[3,3] 7->[3,2,2] 8->[3,3,2]
 __device__ __forceinline__ int step_radix(int levels, int s) {
-  // 1->[1] 2->[2] 3->[3] 4->[2,2] 5->[3,2] 6->[3,3] 7->[3,2,2] 8->[3,3,2]
   const int nsteps = (levels + 2) / 3;
   const int base = levels / nsteps, extra = levels % nsteps;
   return base + (s < extra ? 1 : 0);
 }
 
-// Run all levels of a pass on a tile whose first buffer is `a`; the last radix step
-// is NOT executed (the caller fuses it with its epilogue).  Returns the buffer
-// holding the input of the last step and sets *l_last, *R_last.
+// Run all radix steps of a pass except the last, ping-ponging between a and b.
+// Returns the buffer holding the last step's input; *l_last, *R_last describe it.
 __device__ __forceinline__ float* run_levels_but_last(float* a, float* b, int P, int rows,
-                                                      int levels, int nchunks_all, int* l_last,
+                                                      int levels, int nchunks, int* l_last,
                                                       int* R_last) {
   const int nsteps = (levels + 2) / 3;
   int l = 0;
   for (int s = 0; s < nsteps - 1; ++s) {
     const int R = step_radix(levels, s);
-    radix_step_dispatch(R, a, b, P, rows, l, 0, nchunks_all);
+    radix_step_dispatch(R, a, b, P, rows, l, nchunks);
     __syncthreads();
     float* t = a;
     a = b;
@@ -200,178 +261,185 @@ __device__ __forceinline__ float* run_levels_but_last(float* a, float* b, int P,
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Pass A.  grid (ceil(W/XA) tiles, NB blocks, slices*4), block 256.
-// Tile columns u in [u0 - Hp, u0 + XA) -> local col = u - u0 + Hp  (Hp = H rounded
+// Pass A.  Persistent: each CTA loops over tiles (u-tile, block b, slice*family).
+// Tile columns u in [u0 - Hp, u0 + XA) -> local col = u - u0 + Hp (Hp = H rounded
 // up to 8 so the core starts on a chunk boundary); F outside [0, W) reads as 0.
 // ---------------------------------------------------------------------------
+struct PassATile {
+  int u0, b;
+  long long zs, zf;
+};
+
+__device__ __forceinline__ bool pass_a_tile(long long t, const Geometry& g, int nu, int nf,
+                                            PassATile* pt) {
+  const long long per_z = (long long)nu * g.NB;
+  const long long z = t / per_z;
+  const int rem = (int)(t - z * per_z);
+  pt->b = rem / nu;
+  pt->u0 = (rem - pt->b * nu) * g.XA;
+  pt->zs = z / nf;
+  pt->zf = z - pt->zs * nf;
+  return pt->u0 + g.XA > g.N - pt->b * g.H;    // false: no channel needs it
+}
+
 template <int R>
-__device__ __forceinline__ void pass_a_last_step(const float* in, int P, int Hp, int l, int XA,
-                                                 int u0, int b, const Geometry& g, float* dstR) {
+__device__ __forceinline__ void pass_a_last(const float* in, int P, int Hp, int l,
+                                            const PassATile& pt, const Geometry& g, float* dstR) {
   constexpr int NR = 1 << R;
-  const int nch = 1 << l;
-  const int nchunks = XA / kC;
+  const int nchunks = g.XA / kC;
   const int chunk0 = Hp / kC;
-  const int items = nch * nchunks;   // a single group in the last step
+  const int items = (1 << l) * nchunks;   // a single group in the last step
   const FastDiv fd(nchunks);
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  for (int it = threadIdx.x; it < items; it += kThreads) {
     const int c = fd.div(it);
     const int j = chunk0 + it - c * nchunks;
-    float v[NR][RT<R>::T];
-    load_item<R>(in, P, l, 0, c, j * kC, v);
-    local_fht<R>(v);
-    const int ubase = u0 - Hp + j * kC;
+    const int ubase = pt.u0 - Hp + j * kC;
+    auto epi = [&](float (&v)[NR][RT<R>::T]) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int cf = c * NR + r;                 // final pass-A channel
-      const int ulo = g.N - b * (cf + 1);
-      const int uhi = g.W - cf * b;
-      float* out = dstR + (long long)cf * g.WR + (cf * b - g.N + g.NB);
-      if (ubase >= ulo && ubase + kC <= uhi) {
+      for (int r = 0; r < NR; ++r) {
+        const int cf = c * NR + r;                 // final pass-A channel
+        const int ulo = g.N - pt.b * (cf + 1);
+        const int uhi = g.W - cf * pt.b;
+        float* out = dstR + (long long)cf * g.WR + (cf * pt.b - g.N + g.NB);
+        if (ubase >= ulo && ubase + kC <= uhi) {
 #pragma unroll
-        for (int t = 0; t < kC; ++t) out[ubase + t] = v[r][RT<R>::O + t];
-      } else {
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          const int u = ubase + t;
-          if (u >= ulo && u < uhi) out[u] = v[r][RT<R>::O + t];
-        }
-      }
-    }
-  }
-}
-
-// Fill `rows` x D padded tile rows from global rows (pitch gp) starting at global
-// column g0 (may be negative); columns outside [0, gw) read as 0.  Each thread
-// issues kU independent float4 loads before storing (memory-level parallelism).
-__device__ __forceinline__ void fill_tile(float* tile, int P, int rows, int D, const float* src,
-                                          long long gp, int g0, int gw) {
-  constexpr int kU = 6;
-  const int q4 = D >> 2;
-  const int total = rows * q4;
-  const bool vec = ((g0 & 3) == 0) && ((gp & 3) == 0);
-  const FastDiv fq(q4);
-  for (int e0 = threadIdx.x; e0 < total; e0 += kU * blockDim.x) {
-    float4 v[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int e = e0 + k * blockDim.x;
-      if (e < total) {
-        const int r = fq.div(e);
-        const int u = g0 + (e - r * q4) * 4;
-        const float* rp = src + (long long)r * gp;
-        if (vec && u >= 0 && u + 3 < gw) {
-          v[k] = __ldg(reinterpret_cast<const float4*>(rp + u));
+          for (int t = 0; t < kC; ++t) out[ubase + t] = v[r][RT<R>::O + t];
         } else {
-          v[k].x = (u >= 0 && u < gw) ? rp[u] : 0.0f;
-          v[k].y = (u + 1 >= 0 && u + 1 < gw) ? rp[u + 1] : 0.0f;
-          v[k].z = (u + 2 >= 0 && u + 2 < gw) ? rp[u + 2] : 0.0f;
-          v[k].w = (u + 3 >= 0 && u + 3 < gw) ? rp[u + 3] : 0.0f;
+#pragma unroll
+          for (int t = 0; t < kC; ++t) {
+            const int u = ubase + t;
+            if (u >= ulo && u < uhi) out[u] = v[r][RT<R>::O + t];
+          }
         }
       }
-    }
-#pragma unroll
-    for (int k = 0; k < kU; ++k) {
-      const int e = e0 + k * blockDim.x;
-      if (e < total) {
-        const int r = fq.div(e);
-        const int c4 = (e - r * q4) * 4;
-        *reinterpret_cast<float4*>(tile + (size_t)r * P + pc(c4)) = v[k];
-      }
-    }
+    };
+    item<R>(in, P, l, 0, c, j * kC, epi);
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_fht_a(const float* __restrict__ lin,
-                                               float* __restrict__ R, Geometry g, int P, int f0,
-                                               int nf, long long lin_slice_stride) {
+__global__ void __launch_bounds__(kThreads, 2) k_fht_a(const float* __restrict__ lin,
+                                                       float* __restrict__ R, Geometry g, int P,
+                                                       int f0, int nf, long long lin_slice_stride,
+                                                       long long ntiles) {
   extern __shared__ float smem[];
-  const int b = blockIdx.y;
-  const int zs = blockIdx.z / nf, zf = blockIdx.z % nf;
-  const long long sf = (long long)zs * 4 + f0 + zf;     // output (slice, family)
-  const int XA = g.XA, H = g.H;
+  const int H = g.H;
   const int Hp = (H + kC - 1) / kC * kC;
-  const int u0 = blockIdx.x * XA;
-  if (u0 + XA <= g.N - b * H) return;      // no channel needs these columns
-  const int D = XA + Hp;
-  float* A = smem;
-  float* B = smem + (size_t)H * P;
-  const float* src = lin + zs * lin_slice_stride + ((long long)zf * g.N + (long long)b * H) * g.W;
-  fill_tile(A, P, H, D, src, g.W, u0 - Hp, g.W);
-  __syncthreads();
-  int l_last, R_last;
-  const float* in = run_levels_but_last(A, B, P, H, g.k1, D / kC, &l_last, &R_last);
-  float* dstR = R + ((sf * g.NB + b) * (long long)H) * g.WR;
-  if (R_last == 3) pass_a_last_step<3>(in, P, Hp, l_last, XA, u0, b, g, dstR);
-  else if (R_last == 2) pass_a_last_step<2>(in, P, Hp, l_last, XA, u0, b, g, dstR);
-  else pass_a_last_step<1>(in, P, Hp, l_last, XA, u0, b, g, dstR);
+  const int D = g.XA + Hp;
+  const int nu = (g.W + g.XA - 1) / g.XA;
+  float* buf[2] = {smem, smem + (size_t)H * P};
+  auto src_of = [&](const PassATile& pt) {
+    return lin + pt.zs * lin_slice_stride + (pt.zf * g.N + (long long)pt.b * H) * g.W;
+  };
+  long long t = blockIdx.x;
+  PassATile cur;
+  while (t < ntiles && !pass_a_tile(t, g, nu, nf, &cur)) t += gridDim.x;
+  if (t >= ntiles) return;
+  int fb = 0;                                       // buffer holding the current fill
+  fill_async(buf[fb], P, H, D, src_of(cur), g.W, cur.u0 - Hp, g.W);
+  while (true) {
+    long long tn = t + gridDim.x;                   // next needed tile
+    PassATile nxt;
+    while (tn < ntiles && !pass_a_tile(tn, g, nu, nf, &nxt)) tn += gridDim.x;
+    cp_async_wait<0>();
+    __syncthreads();
+    int l_last, R_last;
+    float* in = run_levels_but_last(buf[fb], buf[fb ^ 1], P, H, g.k1, D / kC, &l_last, &R_last);
+    const int in_idx = (in == buf[0]) ? 0 : 1;
+    // the other buffer is free during the last step: prefetch the next tile there
+    if (tn < ntiles) fill_async(buf[in_idx ^ 1], P, H, D, src_of(nxt), g.W, nxt.u0 - Hp, g.W);
+    const long long sf = cur.zs * 4 + (f0 + cur.zf);
+    float* dstR = R + ((sf * g.NB + cur.b) * (long long)H) * g.WR;
+    if (R_last == 3) pass_a_last<3>(in, P, Hp, l_last, cur, g, dstR);
+    else if (R_last == 2) pass_a_last<2>(in, P, Hp, l_last, cur, g, dstR);
+    else pass_a_last<1>(in, P, Hp, l_last, cur, g, dstR);
+    if (tn >= ntiles) break;
+    __syncthreads();                                 // everyone done reading `in`
+    t = tn;
+    cur = nxt;
+    fb = in_idx ^ 1;
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Pass B.  grid (ceil(N/XB) x-tiles, H channels, slices), block 256.
+// Pass B.  Persistent: each CTA loops over items (x-tile, channel c, slice).
 // Family f = 2*pair + q at tile start xs (q = 0: x0; q = 1: mirrored N - x0 - XB).
 // Rows b in [0,NB) of G_c[b][v], v in [u0 - NBp, u0 + XB), u0 = xs + N; compact R
-// index j' = v - N + NB.  Family 1 runs first and is parked in smem; family 0 then
-// adds the mirrored values (Eq.22 pair), scales and stores.
+// index j' = v - N + NB.  Family 1 is processed first and parked (padded rows);
+// family 0 then adds the mirrored values (Eq.22 pair), scales and stores.
+// Buffers: Fb[1], Fb[0] (family fills), Wk (work), PK (park).
 // ---------------------------------------------------------------------------
+struct PassBItem {
+  int x0, c;
+  long long slice;
+};
+
+__device__ __forceinline__ void pass_b_item(long long t, const Geometry& g, int nx, PassBItem* it) {
+  const long long per_s = (long long)nx * g.H;
+  it->slice = t / per_s;
+  const int rem = (int)(t - it->slice * per_s);
+  it->c = rem / nx;
+  it->x0 = (rem - it->c * nx) * g.XB;
+}
+
 template <int R, bool PARK>
-__device__ __forceinline__ void pass_b_last_step(const float* in, int P, int NBp, int l, int XB,
-                                                 float* park, const float* parked, float* out,
-                                                 int pair, int c, int NB, int x0, float scale,
-                                                 int N, float* stage) {
+__device__ __forceinline__ void pass_b_last(const float* in, int P, int NBp, int l, int NB,
+                                            int XB, float* park, const float* parked, float* out,
+                                            int pair, int c, int x0, float scale, int N,
+                                            float* stage) {
   constexpr int NR = 1 << R;
-  const int nch = 1 << l;
   const int nchunks = XB / kC;
-  const int items = nch * nchunks;
+  const int items = (1 << l) * nchunks;
   const FastDiv fd(nchunks);
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+  for (int it = threadIdx.x; it < items; it += kThreads) {
     const int cc = fd.div(it);
     const int jj = it - cc * nchunks;
-    float v[NR][RT<R>::T];
-    load_item<R>(in, P, l, 0, cc, NBp + jj * kC, v);
-    local_fht<R>(v);
+    auto epi = [&](float (&v)[NR][RT<R>::T]) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int rf = cc * NR + r;               // final row within the channel block
-      if (PARK) {
-#pragma unroll
-        for (int t = 0; t < kC; ++t) park[rf * XB + jj * kC + t] = v[r][RT<R>::O + t];
-      } else {
-        float s[kC];
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          const int i = jj * kC + t;
-          s[t] = scale * (v[r][RT<R>::O + t] + parked[rf * XB + (XB - 1 - i)]);
-        }
-        const int y = c * NB + rf;
-        const int xb = x0 + jj * kC;
-        if (pair == 0) {
-          float* o = out + (long long)y * N + xb;
-          if (xb + kC <= N) {
-            *reinterpret_cast<float4*>(o) = make_float4(s[0], s[1], s[2], s[3]);
-            *reinterpret_cast<float4*>(o + 4) = make_float4(s[4], s[5], s[6], s[7]);
-          } else {
-#pragma unroll
-            for (int t = 0; t < kC; ++t)
-              if (xb + t < N) o[t] = s[t];
-          }
+      for (int r = 0; r < NR; ++r) {
+        const int rf = cc * NR + r;                // final row within the channel block
+        if (PARK) {
+          store8(park + (size_t)rf * P, jj * kC, &v[r][RT<R>::O]);
         } else {
-          // transposed pair: park in the free tile buffer (padded rows), written
-          // out coalesced by pass_b_flush_h after the barrier
+          // mirrored family-1 values: columns XB-1-i for i = jj*8 .. jj*8+7
+          const float* pr = parked + (size_t)rf * P;
+          const int m0 = XB - kC - jj * kC;
+          const float4 a = *reinterpret_cast<const float4*>(pr + pc(m0));
+          const float4 bq = *reinterpret_cast<const float4*>(pr + pc(m0 + 4));
+          const float mir[kC] = {bq.w, bq.z, bq.y, bq.x, a.w, a.z, a.y, a.x};
+          float s[kC];
 #pragma unroll
-          store8(stage + (size_t)rf * P, jj * kC, s);
+          for (int tt = 0; tt < kC; ++tt) s[tt] = scale * (v[r][RT<R>::O + tt] + mir[tt]);
+          const int y = c * NB + rf;
+          const int xb = x0 + jj * kC;
+          if (pair == 0) {
+            float* o = out + (long long)y * N + xb;
+            if (xb + kC <= N) {
+              *reinterpret_cast<float4*>(o) = make_float4(s[0], s[1], s[2], s[3]);
+              *reinterpret_cast<float4*>(o + 4) = make_float4(s[4], s[5], s[6], s[7]);
+            } else {
+#pragma unroll
+              for (int tt = 0; tt < kC; ++tt)
+                if (xb + tt < N) o[tt] = s[tt];
+            }
+          } else {
+            store8(stage + (size_t)rf * P, jj * kC, s);   // transposed by pass_b_flush_h
+          }
         }
       }
-    }
+    };
+    item<R>(in, P, l, 0, cc, NBp + jj * kC, epi);
   }
 }
 
 template <bool PARK>
-__device__ __forceinline__ void pass_b_last(int R, const float* in, int P, int NBp, int l, int XB,
-                                            float* park, const float* parked, float* out, int pair,
-                                            int c, int NB, int x0, float scale, int N, float* stage) {
-  if (R == 3) pass_b_last_step<3, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
-  else if (R == 2) pass_b_last_step<2, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
-  else pass_b_last_step<1, PARK>(in, P, NBp, l, XB, park, parked, out, pair, c, NB, x0, scale, N, stage);
+__device__ __forceinline__ void pass_b_last_dispatch(int R, const float* in, int P, int NBp, int l,
+                                                     int NB, int XB, float* park,
+                                                     const float* parked, float* out, int pair,
+                                                     int c, int x0, float scale, int N,
+                                                     float* stage) {
+  if (R == 3) pass_b_last<3, PARK>(in, P, NBp, l, NB, XB, park, parked, out, pair, c, x0, scale, N, stage);
+  else if (R == 2) pass_b_last<2, PARK>(in, P, NBp, l, NB, XB, park, parked, out, pair, c, x0, scale, N, stage);
+  else pass_b_last<1, PARK>(in, P, NBp, l, NB, XB, park, parked, out, pair, c, x0, scale, N, stage);
 }
 
 // h pair: out[x0 + i][c*NB + r] += stage[r][i]  (stage rows padded like the tiles)
@@ -380,7 +448,7 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
   if ((NB & 3) == 0) {
     const int q = NB >> 2;
     const FastDiv fq(q);
-    for (int e = threadIdx.x; e < XB * q; e += blockDim.x) {
+    for (int e = threadIdx.x; e < XB * q; e += kThreads) {
       const int i = fq.div(e);
       const int r = (e - i * q) * 4;
       if (x0 + i >= N) continue;
@@ -394,7 +462,7 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
     }
   } else {
     const FastDiv fn(NB);
-    for (int e = threadIdx.x; e < XB * NB; e += blockDim.x) {
+    for (int e = threadIdx.x; e < XB * NB; e += kThreads) {
       const int i = fn.div(e);
       const int r = e - i * NB;
       if (x0 + i >= N) continue;
@@ -404,52 +472,79 @@ __device__ __forceinline__ void pass_b_flush_h(const float* stage, int P, int NB
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_fht_b(const float* __restrict__ R,
-                                               float* __restrict__ img, Geometry g, int P,
-                                               int pair, float scale) {
+__global__ void __launch_bounds__(kThreads, 2) k_fht_b(const float* __restrict__ R,
+                                                       float* __restrict__ img, Geometry g, int P,
+                                                       int pair, float scale, long long nitems) {
   extern __shared__ float smem[];
   const int NB = g.NB, XB = g.XB, N = g.N;
   const int NBp = (NB + kC - 1) / kC * kC;
-  const int c = blockIdx.y;
-  const long long slice = blockIdx.z;
-  const int x0 = blockIdx.x * XB;
   const int D = XB + NBp;
-  float* A = smem;
-  float* B = smem + (size_t)NB * P;
-  float* park = B + (size_t)NB * P;       // [NB][XB]
-  float* out = img + slice * (long long)N * N;
-  for (int q = 1; q >= 0; --q) {
+  const int nx = (N + XB - 1) / XB;
+  float* Fb[2] = {smem, smem + (size_t)NB * P};       // family fills (q = 0, 1)
+  float* Wk = smem + (size_t)2 * NB * P;              // work buffer
+  float* PK = smem + (size_t)3 * NB * P;              // park (family 1)
+  auto fill = [&](const PassBItem& it, int q) {
     const int f = 2 * pair + q;
-    const int xs = (q == 0) ? x0 : (N - x0 - XB);
-    const float* src = R + (((slice * 4 + f) * NB) * (long long)g.H + c) * g.WR;
-    fill_tile(A, P, NB, D, src, (long long)g.H * g.WR, xs - NBp + NB, g.WR);
+    const int xs = (q == 0) ? it.x0 : (N - it.x0 - XB);
+    const float* src = R + (((it.slice * 4 + f) * NB) * (long long)g.H + it.c) * g.WR;
+    fill_async(Fb[q], P, NB, D, src, (long long)g.H * g.WR, xs - NBp + NB, g.WR);
+  };
+  long long t = blockIdx.x;
+  if (t >= nitems) return;
+  PassBItem cur;
+  pass_b_item(t, g, nx, &cur);
+  fill(cur, 1);
+  fill(cur, 0);
+  while (true) {
+    float* out = img + cur.slice * (long long)N * N;
+    const long long tn = t + gridDim.x;
+    PassBItem nxt;
+    if (tn < nitems) pass_b_item(tn, g, nx, &nxt);
+    // ---- family 1 -> park ----
+    cp_async_wait<1>();                               // family-1 fill landed
     __syncthreads();
-    int l_last = 0, R_last = 0;
-    const float* in = A;
-    if (g.m > 0) in = run_levels_but_last(A, B, P, NB, g.m, D / kC, &l_last, &R_last);
-    float* stage = (in == A) ? B : A;     // free buffer during the last step
-    if (g.m == 0) {
-      // NB == 1: the single row is the result (no levels)
-      for (int i = threadIdx.x; i < XB; i += blockDim.x) {
-        const float v = in[pc(NBp + i)];
-        if (q == 1) {
-          park[i] = v;
-        } else if (x0 + i < N) {
-          const float sv = scale * (v + park[XB - 1 - i]);
-          if (pair == 0) out[(long long)c * N + x0 + i] = sv;
-          else { float* o = out + (long long)(x0 + i) * N + c; *o = *o + sv; }
-        }
-      }
-    } else if (q == 1) {
-      pass_b_last<true>(R_last, in, P, NBp, l_last, XB, park, nullptr, out, pair, c, NB, x0, scale, N, stage);
-    } else {
-      pass_b_last<false>(R_last, in, P, NBp, l_last, XB, nullptr, park, out, pair, c, NB, x0, scale, N, stage);
-      if (pair == 1) {
-        __syncthreads();
-        pass_b_flush_h(stage, P, NB, XB, c, x0, out, N);
+    {
+      int l_last = 0, R_last = 0;
+      float* in = Fb[1];
+      if (g.m > 0) in = run_levels_but_last(Fb[1], Wk, P, NB, g.m, D / kC, &l_last, &R_last);
+      if (g.m == 0) {
+        for (int i = threadIdx.x; i < XB; i += kThreads) PK[pc(i)] = in[pc(NBp + i)];
+      } else {
+        pass_b_last_dispatch<true>(R_last, in, P, NBp, l_last, NB, XB, PK, nullptr, out, pair,
+                                   cur.c, cur.x0, scale, N, nullptr);
       }
     }
     __syncthreads();
+    if (tn < nitems) fill(nxt, 1);                   // Fb[1] free again
+    // ---- family 0 + pair sum ----
+    if (tn < nitems) cp_async_wait<1>(); else cp_async_wait<0>();
+    __syncthreads();
+    {
+      int l_last = 0, R_last = 0;
+      float* in = Fb[0];
+      if (g.m > 0) in = run_levels_but_last(Fb[0], Wk, P, NB, g.m, D / kC, &l_last, &R_last);
+      float* stage = (in == Wk) ? Fb[0] : Wk;        // free during the last step
+      if (g.m == 0) {
+        for (int i = threadIdx.x; i < XB; i += kThreads) {
+          if (cur.x0 + i >= N) continue;
+          const float sv = scale * (in[pc(NBp + i)] + PK[pc(XB - 1 - i)]);
+          if (pair == 0) out[(long long)cur.c * N + cur.x0 + i] = sv;
+          else { float* o = out + (long long)(cur.x0 + i) * N + cur.c; *o = *o + sv; }
+        }
+      } else {
+        pass_b_last_dispatch<false>(R_last, in, P, NBp, l_last, NB, XB, nullptr, PK, out, pair,
+                                    cur.c, cur.x0, scale, N, stage);
+        if (pair == 1) {
+          __syncthreads();
+          pass_b_flush_h(stage, P, NB, XB, cur.c, cur.x0, out, N);
+        }
+      }
+    }
+    if (tn >= nitems) break;
+    __syncthreads();                                  // Fb[0], Wk, PK reads done
+    fill(nxt, 0);
+    t = tn;
+    cur = nxt;
   }
 }
 
@@ -467,7 +562,16 @@ size_t fht_pass_a_smem(const Geometry& g) {
 
 size_t fht_pass_b_smem(const Geometry& g) {
   const int NBp = (g.NB + kC - 1) / kC * kC;
-  return ((size_t)2 * g.NB * pitch_for(g.XB + NBp) + (size_t)g.NB * g.XB) * sizeof(float);
+  return (size_t)4 * g.NB * pitch_for(g.XB + NBp) * sizeof(float);
+}
+
+static int resident_grid(const void* kernel, size_t smem) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kThreads, smem);
+  if (per < 1) per = 1;
+  return sms * per;
 }
 
 cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, int f0, int nf,
@@ -479,8 +583,9 @@ cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, int f0, in
   const size_t smem = fht_pass_a_smem(g);
   cudaError_t e = cudaFuncSetAttribute(k_fht_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.W + g.XA - 1) / g.XA, g.NB, slices * nf);
-  k_fht_a<<<grid, 256, smem, st>>>(lin, R, g, P, f0, nf, lin_slice_stride);
+  const long long ntiles = (long long)((g.W + g.XA - 1) / g.XA) * g.NB * slices * nf;
+  const long long grid = std::min<long long>(ntiles, resident_grid((const void*)k_fht_a, smem));
+  k_fht_a<<<(unsigned)grid, kThreads, smem, st>>>(lin, R, g, P, f0, nf, lin_slice_stride, ntiles);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
@@ -493,8 +598,9 @@ cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, 
   const size_t smem = fht_pass_b_smem(g);
   cudaError_t e = cudaFuncSetAttribute(k_fht_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((g.N + g.XB - 1) / g.XB, g.H, slices);
-  k_fht_b<<<grid, 256, smem, st>>>(R, img, g, P, pair, scale);
+  const long long nitems = (long long)((g.N + g.XB - 1) / g.XB) * g.H * slices;
+  const long long grid = std::min<long long>(nitems, resident_grid((const void*)k_fht_b, smem));
+  k_fht_b<<<(unsigned)grid, kThreads, smem, st>>>(R, img, g, P, pair, scale, nitems);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
