@@ -133,66 +133,53 @@ __device__ __forceinline__ void local_fht(float (&v)[RT<R>::NR][RT<R>::T]) {
   }
 }
 
+// Intermediate rows are stored shifted right by (their next pre-shift) & 3, so that
+// every item window below is 4-column aligned: virtual column x of row rho lives
+// at physical column x + sh4(rho), sh4 = (c'*b') & 3 for the step that reads it.
+
 // Load the window [col0 - O, col0 - O + T) of the 2^R pre-shifted input rows of
-// item (G, c, chunk at col0): row b read at virtual column col - c*b.  CM = c & 3
-// makes every row's alignment offset (-c*b) & 3 a compile-time constant, so the
-// aligned LDS.128 quads land directly in the item registers (no moves).
-template <int R, int CM>
+// item (G, c, chunk at col0): row b read at virtual column col - c*b, i.e. at
+// physical col - 4*floor(c*b/4) (aligned LDS.128 quads, no register moves).
+template <int R>
 __device__ __forceinline__ void load_item(const float* tile, int P, int l, int G, int c, int col0,
                                           float (&v)[RT<R>::NR][RT<R>::T]) {
   constexpr int NR = RT<R>::NR;
   constexpr int T = RT<R>::T;
 #pragma unroll
   for (int b = 0; b < NR; ++b) {
-    const int o = (4 - ((CM * b) & 3)) & 3;             // (-c*b) & 3, compile-time
     const int row = ((G << R) + b) * (1 << l) + c;
     const float* rp = tile + (size_t)row * P;
-    const int cs = col0 - RT<R>::O - c * b;              // first window column
-    if (cs >= 0) {
-      const int ws = cs - o;                             // 4-aligned
-      constexpr int NQ = (T + 3 + 3) / 4;                // enough quads for any o
-      float w[NQ * 4];
+    const int s = c * b;
+    const int ws = col0 - RT<R>::O - (s & ~3);           // physical, 4-aligned
+    if (ws >= 0) {
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        if (4 * q < T + o) {
-          const float4 f = *reinterpret_cast<const float4*>(rp + pc(ws + 4 * q));
-          w[4 * q] = f.x;
-          w[4 * q + 1] = f.y;
-          w[4 * q + 2] = f.z;
-          w[4 * q + 3] = f.w;
-        }
+      for (int q = 0; q < T / 4; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(rp + pc(ws + 4 * q));
+        v[b][4 * q] = f.x;
+        v[b][4 * q + 1] = f.y;
+        v[b][4 * q + 2] = f.z;
+        v[b][4 * q + 3] = f.w;
       }
-#pragma unroll
-      for (int t = 0; t < T; ++t) v[b][t] = w[t + o];
     } else {
+      const int cs = col0 - RT<R>::O - s;                // virtual window start
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const int col = cs + t;
-        v[b][t] = (col >= 0) ? rp[pc(col)] : 0.0f;
+        v[b][t] = (col >= 0) ? rp[pc(ws + t)] : 0.0f;
       }
     }
   }
 }
 
-// Process one item: load (alignment specialised on c & 3), R register levels,
-// then the epilogue epi(v) with outputs v[r][O + t], t < 8.
-template <int R, int CM, typename Epi>
-__device__ __forceinline__ void item_cm(const float* tile, int P, int l, int G, int c, int col0,
-                                        Epi& epi) {
-  float v[RT<R>::NR][RT<R>::T];
-  load_item<R, CM>(tile, P, l, G, c, col0, v);
-  local_fht<R>(v);
-  epi(v);
-}
+// Process one item: load, R register levels, then the epilogue epi(v) with
+// outputs v[r][O + t], t < 8.
 template <int R, typename Epi>
 __device__ __forceinline__ void item(const float* tile, int P, int l, int G, int c, int col0,
                                      Epi& epi) {
-  switch (c & 3) {
-    case 0: item_cm<R, 0>(tile, P, l, G, c, col0, epi); break;
-    case 1: item_cm<R, 1>(tile, P, l, G, c, col0, epi); break;
-    case 2: item_cm<R, 2>(tile, P, l, G, c, col0, epi); break;
-    default: item_cm<R, 3>(tile, P, l, G, c, col0, epi); break;
-  }
+  float v[RT<R>::NR][RT<R>::T];
+  load_item<R>(tile, P, l, G, c, col0, v);
+  local_fht<R>(v);
+  epi(v);
 }
 
 // Store 8 outputs at columns [col0, col0 + 8) of a padded row (2 x STS.128).
@@ -201,12 +188,47 @@ __device__ __forceinline__ void store8(float* rp, int col0, const float* s) {
   *reinterpret_cast<float4*>(rp + pc(col0 + 4)) = make_float4(s[4], s[5], s[6], s[7]);
 }
 
+// Store 8 outputs at physical columns [col0 + off, col0 + off + 8), off in 0..3,
+// col0 a multiple of 8 (pieces never straddle a 32-column pad boundary).
+__device__ __forceinline__ void store8_off(float* rp, int col0, int off, const float* s) {
+  float* p = rp + pc(col0);          // 8-aligned group: pc is contiguous over 8 columns
+  switch (off) {
+    case 0:
+      *reinterpret_cast<float4*>(p) = make_float4(s[0], s[1], s[2], s[3]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(s[4], s[5], s[6], s[7]);
+      break;
+    case 1:
+      p[1] = s[0];
+      *reinterpret_cast<float2*>(p + 2) = make_float2(s[1], s[2]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(s[3], s[4], s[5], s[6]);
+      rp[pc(col0 + 8)] = s[7];
+      break;
+    case 2:
+      *reinterpret_cast<float2*>(p + 2) = make_float2(s[0], s[1]);
+      *reinterpret_cast<float4*>(p + 4) = make_float4(s[2], s[3], s[4], s[5]);
+      *reinterpret_cast<float2*>(rp + pc(col0 + 8)) = make_float2(s[6], s[7]);
+      break;
+    default: {
+      p[3] = s[0];
+      *reinterpret_cast<float4*>(p + 4) = make_float4(s[1], s[2], s[3], s[4]);
+      float* q = rp + pc(col0 + 8);
+      *reinterpret_cast<float2*>(q) = make_float2(s[5], s[6]);
+      q[2] = s[7];
+      break;
+    }
+  }
+}
+
 // One intermediate radix step in shared memory: in -> out (padded, pitch P).
+// The output row rho is written shifted by (its pre-shift in the next step) & 3;
+// the next step has l' = l + R levels done and radix Rn.
 template <int R>
-__device__ void radix_step_smem(const float* in, float* out, int P, int rows, int l, int nchunks) {
+__device__ void radix_step_smem(const float* in, float* out, int P, int rows, int l, int Rn,
+                                int nchunks) {
   constexpr int NR = 1 << R;
   const int nch = 1 << l;
   const int items = (rows >> (l + R)) * nch * nchunks;
+  const int ln = l + R;
   const FastDiv fd(nchunks);
   for (int it = threadIdx.x; it < items; it += kThreads) {
     const int gc = fd.div(it);
@@ -215,18 +237,22 @@ __device__ void radix_step_smem(const float* in, float* out, int P, int rows, in
     const int G = gc >> l;
     auto epi = [&](float (&v)[NR][RT<R>::T]) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-        store8(out + (size_t)((G << (l + R)) + c * NR + r) * P, j * kC, &v[r][RT<R>::O]);
+      for (int r = 0; r < NR; ++r) {
+        const int rho = (G << (l + R)) + c * NR + r;
+        const int cn = rho & ((1 << ln) - 1);                 // next step's channel
+        const int bn = (rho >> ln) & ((1 << Rn) - 1);         // next step's block
+        store8_off(out + (size_t)rho * P, j * kC, (cn * bn) & 3, &v[r][RT<R>::O]);
+      }
     };
     item<R>(in, P, l, G, c, j * kC, epi);
   }
 }
 
 __device__ __forceinline__ void radix_step_dispatch(int R, const float* in, float* out, int P,
-                                                    int rows, int l, int nchunks) {
-  if (R == 3) radix_step_smem<3>(in, out, P, rows, l, nchunks);
-  else if (R == 2) radix_step_smem<2>(in, out, P, rows, l, nchunks);
-  else radix_step_smem<1>(in, out, P, rows, l, nchunks);
+                                                    int rows, int l, int Rn, int nchunks) {
+  if (R == 3) radix_step_smem<3>(in, out, P, rows, l, Rn, nchunks);
+  else if (R == 2) radix_step_smem<2>(in, out, P, rows, l, Rn, nchunks);
+  else radix_step_smem<1>(in, out, P, rows, l, Rn, nchunks);
 }
 
 // Split `levels` into radix steps of at most 3 levels: radix of step s.
@@ -246,7 +272,7 @@ __device__ __forceinline__ float* run_levels_but_last(float* a, float* b, int P,
   int l = 0;
   for (int s = 0; s < nsteps - 1; ++s) {
     const int R = step_radix(levels, s);
-    radix_step_dispatch(R, a, b, P, rows, l, nchunks);
+    radix_step_dispatch(R, a, b, P, rows, l, step_radix(levels, s + 1), nchunks);
     __syncthreads();
     float* t = a;
     a = b;
