@@ -299,6 +299,7 @@ def run_fbp(args):
                        "N": N, "slices_per_gpu_per_step": B, "coeffs": "dc0 M=Q=3",
                        "l2": f"inputs {B * 4 * N * 2 * N * 4 / 2**30:.1f} GiB/step per GPU > 126 MB L2 (no flush needed)",
                        "level_split": f"k1={info['k1']} m={info['m']}",
+                       "schedule": plan.path(),
                        "parallelism": f"slices sharded over {world} GPU(s), no collective"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

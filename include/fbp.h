@@ -100,6 +100,10 @@ FBP_API fbp_status fbp_fht_backproject(const fbp_plan* plan, const float* lin, f
  * projection with weight w = 1/N (reading R7).
  *   sino: device [batch][4][N][2N];  image: device [batch][N][N].
  * Not required to equal fbp_fht_backproject(fbp_iir_filter(.), 1/N) bitwise.
+ * On the fused fast path (fbp_plan_path) the anticausal recursion's carry into
+ * each tile of X samples sums the next D tiles only; D is the smallest tile
+ * count whose dropped impulse-response tail is <= 1e-12 of its l1 norm
+ * (reading R22).  Otherwise the recursion is exact.
  */
 FBP_API fbp_status fbp_reconstruct(const fbp_plan* plan, const float* sino, float* image, int batch,
                            void* cuda_stream);
@@ -133,6 +137,14 @@ FBP_API long long fbp_plan_launch_count(const fbp_plan* plan);
  */
 FBP_API fbp_status fbp_plan_profile(fbp_plan* plan, int enable);
 FBP_API fbp_status fbp_plan_kernel_times(fbp_plan* plan, double* ms, long long* launches, int kinds);
+
+/*
+ * Schedule chosen for this plan.  *fast = 1: fused IIR + FHT pass-A sweep and
+ * pair-wise pass B (N in {512, 1024, 2048}, M <= 3, Q <= 3, coefficient tail
+ * bound met); 0: separate IIR and two-pass FHT kernels.  *lookahead_tiles = D,
+ * *tile_width = X of the sweep (0 when not fast).  Any pointer may be NULL.
+ */
+FBP_API fbp_status fbp_plan_path(const fbp_plan* plan, int* fast, int* lookahead_tiles, int* tile_width);
 
 /* Level split chosen for this plan: *k1 levels in pass A, *m levels in pass B. */
 FBP_API fbp_status fbp_plan_info(const fbp_plan* plan, int* n, int* k1, int* m, int* slices_per_group,

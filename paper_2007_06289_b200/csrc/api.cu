@@ -31,6 +31,11 @@ struct fbp_plan {
   float* h_in[2] = {nullptr, nullptr};
   float* h_out[2] = {nullptr, nullptr};
   cudaStream_t s_copy = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  // fast path (sweep.cu): fused IIR + pass-A sweep and pair-wise pass B
+  bool fast = false;
+  SweepGeom sg{};
+  SweepIir si{};
+  int* counter = nullptr;   // sweep work-queue counter (device)
   mutable long long launches = 0;
   // per-kernel event timing (fbp_plan_profile)
   mutable bool profiling = false;
@@ -176,6 +181,29 @@ cudaError_t run_backproject(const fbp_plan* p, const float* lin, float* img, int
   return timed(p, 2, st, [&] { return launch_fht_pass_b(p->R, img, slices, 1, scale, p->g, st, launches); });
 }
 
+// Fast path: sweep (IIR fused or not) into plan->R, then the two Eq.22 pairs.
+cudaError_t run_fast(const fbp_plan* p, const float* lin, float* img, int batch, float scale,
+                     bool iir, cudaStream_t st, int* launches) {
+  const Geometry& g = p->g;
+  const long long lin_elems = 4LL * g.N * g.W;
+  const long long img_elems = (long long)g.N * g.N;
+  for (int s0 = 0; s0 < batch; s0 += p->group) {
+    const int ns = std::min(p->group, batch - s0);
+    cudaError_t e = timed(p, 1, st, [&] {
+      return launch_sweep_a(lin + s0 * lin_elems, p->R, ns, 0, 4, lin_elems, p->sg, p->si, iir,
+                            p->counter, st, launches);
+    });
+    if (e != cudaSuccess) return e;
+    for (int pair = 0; pair < 2; ++pair) {
+      e = timed(p, 2, st, [&] {
+        return launch_pair_b(p->R, img + s0 * img_elems, ns, pair, scale, p->sg, st, launches);
+      });
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
 cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, int batch,
                             cudaStream_t st, int* launches) {
   const Geometry& g = p->g;
@@ -183,6 +211,7 @@ cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, in
   const long long img_elems = (long long)g.N * g.N;
   const float w = 1.0f / (float)g.N;  // exact power of two (R7)
   const long long fam_elems = (long long)g.N * g.W;
+  if (p->fast) return run_fast(p, sino, img, batch, w, true, st, launches);
   if (p->per_family) {
     // Large N: one line family at a time, so that the filtered family (N x 2N
     // fp32, 32 MiB at N = 2048) is consumed by pass A while it is L2-resident;
@@ -312,11 +341,73 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     put(lm.data() + (size_t)j * kMaxOrder * kMaxOrder, Pk);
   }
 
+  // ---- fast path: sweep kernels (M, Q <= 3; N in the supported set; the
+  //      anticausal look-ahead D tiles long enough for a 1e-12 tail, R22) ----
+  if (sweep_supported(n) && m <= 3 && q <= 3) {
+    SweepGeom& sg = p->sg;
+    sg.N = n;
+    sg.W = 2 * n;
+    sg.NB = p->g.NB;
+    sg.H = p->g.H;
+    sg.WR = p->g.WR;
+    sg.X = 4096 / sg.H;
+    sg.nt = sg.W / sg.X;
+    sg.P = 4;
+    sg.XB = 128;
+    // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
+    const int K = 1 << 16;
+    std::vector<double> h(K, 0.0);
+    for (int i = 0; i < K; ++i) {
+      double v = (i < m) ? b[i] : 0.0;
+      for (int k = 1; k <= q && k <= i; ++k) v -= a[k - 1] * h[i - k];
+      h[i] = v;
+    }
+    std::vector<double> tail(K + 1, 0.0);
+    for (int i = K - 1; i >= 0; --i) tail[i] = tail[i + 1] + std::fabs(h[i]);
+    int D = 0;
+    for (int d = 1; d <= 16; ++d) {
+      const int lag = std::max(0, d * sg.X - 2);
+      if (lag < K && tail[lag] <= 1e-12 * tail[0]) {
+        D = d;
+        break;
+      }
+    }
+    if (D > 0 && std::isfinite(tail[0])) {
+      sg.D = D;
+      SweepIir& si = p->si;
+      auto dup = [](double v) { return make_float2((float)v, (float)v); };
+      double bb[3] = {0, 0, 0}, aa[3] = {0, 0, 0};
+      for (int i = 0; i < m; ++i) bb[i] = b[i];
+      for (int i = 0; i < q; ++i) aa[i] = a[i];
+      si.beta = dup(bb[0] + bb[1] + bb[2]);
+      si.c0 = dup(-(bb[1] + bb[2]));
+      si.c1 = dup(-bb[2]);
+      si.na1 = dup(-aa[0]);
+      si.na2 = dup(-aa[1]);
+      si.na3 = dup(-aa[2]);
+      std::vector<double> A3, Pm;
+      companion(3, aa, A3);
+      auto put = [&](float2* dst, long long e) {
+        matpow(3, A3, e, Pm);
+        for (int i = 0; i < 9; ++i) dst[i] = dup(Pm[(size_t)i]);
+      };
+      put(si.M1, 32);
+      put(si.M2, 64);
+      put(si.MX, sg.X);
+      put(si.M16, 16);
+      for (int i = 0; i < 32; ++i) {
+        matpow(3, A3, i + 1, Pm);
+        for (int mm = 0; mm < 3; ++mm) si.G[i][mm] = dup(Pm[(size_t)mm]);
+      }
+      p->fast = true;
+    }
+  }
+
   // ---- workspace, sized for a group of slices ----
   const Geometry& g = p->g;
-  const size_t f_slice = (size_t)4 * g.N * g.W * sizeof(float);
+  const size_t f_slice = p->fast ? 0 : (size_t)4 * g.N * g.W * sizeof(float);
   const size_t r_slice = (size_t)4 * g.NB * g.H * g.WR * sizeof(float);
-  const size_t budget = (size_t)256 << 20;
+  const size_t budget = p->fast ? ((size_t)1 << 30) : ((size_t)256 << 20);
   long long grp = (long long)(budget / (f_slice + r_slice));
   grp = std::max<long long>(1, std::min<long long>(grp, max_batch));
   grp = std::min<long long>(grp, 16383);
@@ -324,7 +415,9 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   p->per_family = false;  // measured slower (r01 v2c): launch granularity outweighs L2 reuse
   p->F_bytes = f_slice * p->group;
   p->R_bytes = r_slice * p->group;
-  if (cudaMalloc(&p->F, p->F_bytes) != cudaSuccess || cudaMalloc(&p->R, p->R_bytes) != cudaSuccess ||
+  if ((p->F_bytes && cudaMalloc(&p->F, p->F_bytes) != cudaSuccess) ||
+      cudaMalloc(&p->R, p->R_bytes) != cudaSuccess ||
+      cudaMalloc(&p->counter, 16) != cudaSuccess ||
       cudaMalloc(&p->lane_mats, lm.size() * sizeof(float)) != cudaSuccess) {
     cudaGetLastError();
     fbp_plan_destroy(p);
@@ -351,6 +444,7 @@ void fbp_plan_destroy(fbp_plan* p) {
   DeviceGuard guard(p->device);
   cudaFree(p->F);
   cudaFree(p->R);
+  cudaFree(p->counter);
   cudaFree(p->lane_mats);
   for (int i = 0; i < 2; ++i) {
     cudaFree(p->d_in[i]);
@@ -392,6 +486,12 @@ fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image
   int launches = 0;
   const long long lin_elems = 4LL * p->g.N * p->g.W;
   const long long img_elems = (long long)p->g.N * p->g.N;
+  if (p->fast) {
+    cudaError_t e = run_fast(p, lin, image, batch, scale, false, (cudaStream_t)stream, &launches);
+    p->launches = launches;
+    if (e != cudaSuccess) return cuda_fail(e, "fbp_fht_backproject");
+    return FBP_OK;
+  }
   for (int s0 = 0; s0 < batch; s0 += p->group) {
     const int ns = std::min(p->group, batch - s0);
     cudaError_t e = run_backproject(p, lin + s0 * lin_elems, image + s0 * img_elems, ns, scale,
@@ -560,6 +660,14 @@ fbp_status fbp_plan_kernel_times(fbp_plan* p, double* ms, long long* launches, i
   }
   p->recs.clear();
   if (err != cudaSuccess) return cuda_fail(err, "fbp_plan_kernel_times");
+  return FBP_OK;
+}
+
+fbp_status fbp_plan_path(const fbp_plan* p, int* fast, int* lookahead_tiles, int* tile_width) {
+  if (!p) return fail(FBP_ERR_PARAM, "plan is NULL");
+  if (fast) *fast = p->fast ? 1 : 0;
+  if (lookahead_tiles) *lookahead_tiles = p->fast ? p->sg.D : 0;
+  if (tile_width) *tile_width = p->fast ? p->sg.X : 0;
   return FBP_OK;
 }
 

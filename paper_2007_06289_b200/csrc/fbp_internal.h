@@ -44,6 +44,42 @@ struct Geometry {
   int iir_mc;  // number of difference-form feedforward taps c_k (M - 1)
 };
 
+// ---------------------------------------------------------------------------
+// Fast path (sweep.cu): fused IIR + FHT levels 1..k1 as a sweep along s, and the
+// pair-wise pass B.  Orders M <= 3, Q <= 3 (the paper's M = Q = 3); all float2
+// entries are duplicated (v, v) so that both lanes of an f32x2 op see the same
+// coefficient.
+struct SweepIir {
+  float2 beta, c0, c1;        // difference-form feedforward: beta x + c0 D[n] + c1 D[n-1]
+  float2 na1, na2, na3;       // -a_1, -a_2, -a_3
+  float2 M1[9];               // A^32 (row-major 3x3, companion matrix of A(z))
+  float2 M2[9];               // A^64
+  float2 MX[9];               // A^X   (one tile)
+  float2 M16[9];              // A^16
+  float2 G[32][3];            // G[i][m] = (A^(i+1))_{0m}
+};
+
+struct SweepGeom {
+  int N, W, NB, H, WR;
+  int X;      // pass-A tile width (H * X = 4096)
+  int nt;     // tiles per linogram row, W / X
+  int D;      // look-ahead tiles for the anticausal carry (plan: tail bound)
+  int P;      // L2 prefetch distance in tiles
+  int XB;     // pass-B x-tile width
+};
+
+// Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at
+// lin + s*lin_slice_stride + fi*N*W), output R[(s*4 + f0 + fi)].  `counter` is a
+// device int the launcher zeroes (work queue).  iir=false: plain FHT levels.
+cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int nf,
+                           long long lin_slice_stride, const SweepGeom& g, const SweepIir& k,
+                           bool iir, int* counter, cudaStream_t st, int* launches);
+cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, float scale,
+                          const SweepGeom& g, cudaStream_t st, int* launches);
+bool sweep_supported(int N);
+size_t sweep_a_smem(const SweepGeom& g);
+size_t pair_b_smem(const SweepGeom& g);
+
 // Kernel launchers (kernels.cu).  All asynchronous on `st`; return the launch error.
 // lane_mats: device [32][8*8], lane_mats[j] = A^(L*j).
 cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const Geometry& g,

@@ -1,0 +1,820 @@
+// Fast path of the hot path:
+//
+//   k_sweep_a : recursive ramp filter (§3 Eq.12-13) fused with the
+//               first k1 FHT levels (§4.4), one CTA per
+//               (slice, family, block of H = 2^k1 linogram rows), sweeping along s
+//               in tiles of X columns.  The linogram is read from HBM once; the
+//               filtered rows F never leave shared memory.
+//   k_pair_b  : the last m FHT levels of an Eq.22 family pair,
+//               mirror-add, weight and store.
+//
+// IIR in the sweep.  Every row is split into 32-sample chunks (TPR = X/32 chunks
+// of a row per tile, one per thread).  Zero-state sweeps of both directions run
+// packed in f32x2 (.x causal at sample i, .y anticausal at sample 31-i); chunk
+// carries are combined by a Kogge-Stone scan over the TPR chunks of the row with
+// A^32, A^64.  The causal carry into a tile is exact (the sweep goes left to
+// right; each row is zero left of N - t, R2 of DESIGN.md).  The anticausal carry
+// into tile j is sum_{i=1..D} (A^X)^(i-1) agg[j+i], agg[t] being the anticausal
+// state at the left edge of tile t produced by the inputs inside tile t; tiles
+// beyond j + D are dropped, and D is chosen by the plan so that the dropped tail
+// of the impulse response is below 1e-12 of its l1 norm (R22).  The
+// look-ahead tiles are read one tile ahead with plain loads (an L2 prefetch issued
+// P tiles earlier brings them on chip); each tile is later landed a second time
+// (L2 hit) for the exact local pass.
+//
+// FHT items.  A radix-2^R step after l levels computes, for 2^R consecutive
+// blocks of 2^l rows and one channel c (PAPER.md recursion):
+//   out[G*2^(l+R) + c*2^R + r'][u] = sum_{b'<2^R} in[(G*2^R + b')*2^l + c][u - c*b' - d^(R)_{r'}(b')]
+// Each thread owns one item (2^R rows x C columns) per step: it loads the 2^R
+// pre-shifted input windows with LDS.128 (rows are stored shifted right by their
+// next pre-shift mod 4, so every window is 16-byte aligned), runs R levels in
+// registers with compile-time shifts and stores C columns per output row.  Halo
+// columns of every step's input are carried from tile to tile, so no level is
+// recomputed for halos.
+#include "fbp_internal.h"
+
+#include <algorithm>
+
+namespace fbp {
+
+namespace {
+
+extern __shared__ float sm[];
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ float4 ld4(int off) { return *reinterpret_cast<const float4*>(sm + off); }
+__device__ __forceinline__ void st4(int off, float4 v) { *reinterpret_cast<float4*>(sm + off) = v; }
+
+__device__ __forceinline__ void cp16(int soff, const float* g, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sm + soff);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
+
+__device__ __forceinline__ void prefetch_l2(const float* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Row pitch (floats) for a row of at least w floats: a multiple of 4 whose quad
+// count is odd, so that 8 consecutive rows map the same column to 8 distinct
+// 4-bank groups (conflict-free LDS/STS.128 for "8 rows x 1 quad" access).
+__host__ __device__ constexpr int pitch4(int w) { return (((w + 3) / 4) | 1) * 4; }
+
+// Pass-B step-2 input halo: the window offset O2 plus the largest pre-shift
+// (2^R1 - 1)(2^R2 - 1) rounded down to quads, then rounded up to the step-1 item
+// width so that step 1 tiles [0, HS + XB) exactly.
+__host__ __device__ constexpr int pb_halo(int R1, int R2) {
+  return ((((R2 == 3) ? 8 : 4) + 4 * ((((1 << R1) - 1) * ((1 << R2) - 1)) / 4)) + ((R1 == 3) ? 4 : 8) - 1) /
+         ((R1 == 3) ? 4 : 8) * ((R1 == 3) ? 4 : 8);
+}
+
+// Register item geometry: radix 2^R, C output columns; halo quads HQ >= (2^R-1)/4,
+// window T = C + O columns with the outputs at window offset O.
+template <int R, int C>
+struct It {
+  static constexpr int NR = 1 << R;
+  static constexpr int HQ = (NR - 1 + 3) / 4;
+  static constexpr int O = 4 * HQ;
+  static constexpr int T = C + O;
+};
+
+// Load the NR pre-shifted windows of an item.  `w0` = float offset of the window
+// start (virtual column col0 - O) of input row b' = 0; row b' lives at
+// w0 + b'*rowstep, pre-shift c*b' (the physical shift (c*b') & 3 was applied by
+// the producer, so the physical window starts 4*floor(c*b'/4) columns left).
+template <int R, int C>
+__device__ __forceinline__ void item_load(int w0, int rowstep, int c,
+                                          float (&v)[It<R, C>::NR][It<R, C>::T]) {
+  constexpr int NR = It<R, C>::NR, T = It<R, C>::T;
+  int cb = 0;
+#pragma unroll
+  for (int b = 0; b < NR; ++b) {
+    const int off = w0 + b * rowstep - (cb & ~3);
+    cb += c;
+#pragma unroll
+    for (int q = 0; q < T / 4; ++q) {
+      const float4 f = ld4(off + 4 * q);
+      v[b][4 * q] = f.x;
+      v[b][4 * q + 1] = f.y;
+      v[b][4 * q + 2] = f.z;
+      v[b][4 * q + 3] = f.w;
+    }
+  }
+}
+
+// R levels in registers (natural recursion, compile-time shifts), computing at each
+// level only the window columns the outputs [O, T) depend on.
+//   level h -> 2h:  w[blk + y'][t] = v[blk + lo][t] + v[blk + h + lo][t - ceil(y'/2)],
+//   lo = floor(y'/2)  (negative shift direction)
+template <int R, int C>
+__device__ __forceinline__ void item_fht(float (&v)[It<R, C>::NR][It<R, C>::T]) {
+  constexpr int NR = It<R, C>::NR, T = It<R, C>::T, O = It<R, C>::O;
+#pragma unroll
+  for (int lvl = 0; lvl < R; ++lvl) {
+    const int h = 1 << lvl;
+    const int lb = O - ((1 << R) - (1 << (lvl + 1)));
+    float w[NR][T];
+#pragma unroll
+    for (int y = 0; y < NR; ++y) {
+      const int blk = y & ~(2 * h - 1);
+      const int yp = y - blk;
+      const int lo = yp >> 1;
+      const int sh = (yp + 1) >> 1;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        if (t >= lb) w[y][t] = (t >= sh) ? v[blk + lo][t] + v[blk + h + lo][t - sh] : v[blk + lo][t];
+      }
+    }
+#pragma unroll
+    for (int y = 0; y < NR; ++y)
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        if (t >= lb) v[y][t] = w[y][t];
+  }
+}
+
+// ---------------------------------------------------------------- IIR pieces
+struct P3 {   // a 3-state pair: .x causal, .y anticausal
+  float2 s0, s1, s2;
+};
+
+__device__ __forceinline__ P3 mv(const float2 (&M)[9], const P3& v) {
+  P3 o;
+  o.s0 = __fmul2_rn(M[0], v.s0);
+  o.s0 = __ffma2_rn(M[1], v.s1, o.s0);
+  o.s0 = __ffma2_rn(M[2], v.s2, o.s0);
+  o.s1 = __fmul2_rn(M[3], v.s0);
+  o.s1 = __ffma2_rn(M[4], v.s1, o.s1);
+  o.s1 = __ffma2_rn(M[5], v.s2, o.s1);
+  o.s2 = __fmul2_rn(M[6], v.s0);
+  o.s2 = __ffma2_rn(M[7], v.s1, o.s2);
+  o.s2 = __ffma2_rn(M[8], v.s2, o.s2);
+  return o;
+}
+
+// scalar 3x3 matvec using the .x lane of the duplicated matrix: acc + M v
+__device__ __forceinline__ void mv1(const float2 (&M)[9], const float (&v)[3], float (&acc)[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float s = acc[i];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s = fmaf(M[3 * i + j].x, v[j], s);
+    acc[i] = s;
+  }
+}
+
+// Zero-state sweeps of one 32-sample chunk, packed: .x causal at sample i (left to
+// right), .y anticausal at sample 31 - i (right to left).  Eq.13 with difference-
+// form feedforward (R16): u = beta x + c0 D[n] + c1 D[n-1], D[n] = x[n] - x[n-1]
+// (anticausal: E[n] = x[n] - x[n+1], E[n+1]).  xl = x[-1], x[-2]; xr = x[32], x[33].
+template <bool BETA>
+__device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, float xl1, float xr0,
+                                            float xr1, const SweepIir& k, float2 (&yp)[32]) {
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+  float2 xprev = make_float2(xl0, xr0);
+  float2 dprev = make_float2(xl0 - xl1, xr0 - xr1);
+  float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float2 xx = make_float2(x[i], x[31 - i]);
+    const float2 d = __ffma2_rn(m1, xprev, xx);
+    float2 u = __fmul2_rn(k.c1, dprev);
+    u = __ffma2_rn(k.c0, d, u);
+    if (BETA) u = __ffma2_rn(k.beta, xx, u);
+    float2 v = __ffma2_rn(k.na3, y3, u);
+    v = __ffma2_rn(k.na2, y2, v);
+    v = __ffma2_rn(k.na1, y1, v);
+    y3 = y2;
+    y2 = y1;
+    y1 = v;
+    dprev = d;
+    xprev = xx;
+    yp[i] = v;
+  }
+}
+
+// Anticausal zero-state state at the left edge of a 32-sample chunk (true u: the
+// feedforward reads x[32], x[33]).  Packed halves: .x over samples [0,16), .y over
+// [16,32); the chunk state = lo + A^16 hi.
+template <bool BETA>
+__device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], float xn0, float xn1,
+                                                       const SweepIir& k, float (&va)[3]) {
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+  float2 xprev = make_float2(x[16], xn0);
+  float2 dprev = make_float2(x[16] - x[17], xn0 - xn1);
+  float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 xx = make_float2(x[15 - i], x[31 - i]);
+    const float2 d = __ffma2_rn(m1, xprev, xx);
+    float2 u = __fmul2_rn(k.c1, dprev);
+    u = __ffma2_rn(k.c0, d, u);
+    if (BETA) u = __ffma2_rn(k.beta, xx, u);
+    float2 v = __ffma2_rn(k.na3, y3, u);
+    v = __ffma2_rn(k.na2, y2, v);
+    v = __ffma2_rn(k.na1, y1, v);
+    y3 = y2;
+    y2 = y1;
+    y1 = v;
+    dprev = d;
+    xprev = xx;
+  }
+  const float hi[3] = {y1.y, y2.y, y3.y};
+  va[0] = y1.x;
+  va[1] = y2.x;
+  va[2] = y3.x;
+  mv1(k.M16, hi, va);
+}
+
+__device__ __forceinline__ float2 shfl_up2(float2 v, int d) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+
+}  // namespace
+
+// ===========================================================================
+// Pass A sweep.  Threads NT = H*X/32 = 128.  Shared memory (floats):
+//   F0, F1 : H x PF  filtered tile (double buffer; landing target), virtual core
+//            columns [HF, HF+X), halo [0, HF) = previous tile's last HF columns
+//   S1     : H x PS  step-1 output, core [HS, HS+X), halo [0, HS)
+//   ring   : (D+1) x H x 4  anticausal tile aggregates
+// ===========================================================================
+template <int H, int X, bool IIR, bool BETA>
+__global__ void __launch_bounds__(H * X / 32)
+    k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
+              int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter) {
+  constexpr int NT = H * X / 32;
+  constexpr int TPR = X / 32;                 // chunks (threads) per row in the IIR
+  constexpr int R2 = (H == 64) ? 3 : 2;       // k1 = 3 + R2
+  constexpr int C1 = 4;
+  constexpr int C2 = (R2 == 3) ? 4 : 8;
+  constexpr int O2 = It<R2, C2>::O;
+  constexpr int NR2 = 1 << R2;
+  constexpr int HF = 8;                        // step-1 input halo (>= 7)
+  constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);   // step-2 input halo
+  constexpr int PF = pitch4(HF + X + 4);
+  constexpr int PS = pitch4(HS + X + 4);
+  constexpr int oF0 = 0, oF1 = H * PF, oS = 2 * H * PF, oRing = oS + H * PS;
+  static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
+
+  const int tid = threadIdx.x;
+  const int D = g.D;
+  int* s_item = reinterpret_cast<int*>(sm + oRing + (D + 1) * H * 4);
+  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
+  const long long nsf = (long long)slices * nf;
+  const long long nitems = nsf * NB;
+  // IIR roles: a quarter-warp = 8 rows x the same chunk (conflict-free), the TPR
+  // chunks of a row sit 8 lanes apart in one warp.
+  const int iq = (tid >> 3) % TPR;
+  const int ir = (tid & 7) + 8 * (tid / (8 * TPR));
+  const int lane = tid & 31;
+
+  while (true) {
+    __syncthreads();
+    if (tid == 0) *s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long item = *s_item;
+    if (item >= nitems) break;
+    const int b = NB - 1 - (int)(item / nsf);            // longest sweeps first
+    const long long sfi = item - (long long)(NB - 1 - b) * nsf;
+    const long long s = sfi / nf;
+    const int fi = (int)(sfi - s * nf);
+    const int f = f0 + fi;
+    const float* src = lin + s * lin_slice_stride + ((long long)fi * N + (long long)b * H) * W;
+    float* dstR = Rout + (((s * 4 + f) * NB + b) * (long long)H) * WR;
+    // First tile with an output pass B reads: every stored R column u >= N - b*H
+    // depends on F at u - (H-1) >= N - (b+1)H + 1 only.  The sweep starts D tiles
+    // earlier (warm-up tiles: IIR only) so that the causal carry into tile j0
+    // holds every input within D*X samples -- the same tail bound as the
+    // anticausal look-ahead (R22); linogram rows need not be zero left of N - t
+    // (noisy inputs, configs 2, 4, 5).
+    const int j0 = (N - (b + 1) * H + 1) / X;
+    const int jst = IIR ? max(0, j0 - D) : j0;
+
+    // landing of tile jt into F buffer `ofb` (IIR: with one quad of neighbours each side)
+    auto land = [&](int ofb, int jt) {
+      constexpr int NQ = IIR ? (X + 8) / 4 : X / 4;
+      constexpr int c0 = IIR ? HF - 4 : HF;
+      const int g0 = jt * X - (IIR ? 4 : 0);
+      for (int e = tid; e < H * NQ; e += NT) {
+        const int r = e / NQ, qd = e - r * NQ;
+        const int gc = g0 + 4 * qd;
+        const bool ok = (gc >= 0) && (gc < W);
+        cp16(ofb + r * PF + c0 + 4 * qd, ok ? src + (long long)r * W + gc : src, ok);
+      }
+      cp_commit();
+    };
+
+    // look-ahead: anticausal aggregate of tile jt from registers -> ring
+    auto la_finish = [&](int jt, const float (&lx)[32], float ln0, float ln1) {
+      float va[3];
+      // right neighbours of this chunk: next chunk's first two samples (or next tile's)
+      const float p0 = __shfl_down_sync(0xffffffffu, lx[0], 8);
+      const float p1 = __shfl_down_sync(0xffffffffu, lx[1], 8);
+      const float xn0 = (iq == TPR - 1) ? ln0 : p0;
+      const float xn1 = (iq == TPR - 1) ? ln1 : p1;
+      chunk_anticausal_state<BETA>(lx, xn0, xn1, k, va);
+      // suffix combine over the row's chunks: agg = sum_q (A^32)^q va_q
+      P3 S;
+      S.s0 = make_float2(va[0], 0.f);
+      S.s1 = make_float2(va[1], 0.f);
+      S.s2 = make_float2(va[2], 0.f);
+#pragma unroll
+      for (int st = 0; (1 << st) < TPR; ++st) {
+        const int off = 8 << st;
+        P3 o;
+        o.s0 = make_float2(__shfl_down_sync(0xffffffffu, S.s0.x, off), 0.f);
+        o.s1 = make_float2(__shfl_down_sync(0xffffffffu, S.s1.x, off), 0.f);
+        o.s2 = make_float2(__shfl_down_sync(0xffffffffu, S.s2.x, off), 0.f);
+        const P3 t = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
+        if (iq + (1 << st) < TPR) {
+          S.s0.x += t.s0.x;
+          S.s1.x += t.s1.x;
+          S.s2.x += t.s2.x;
+        }
+      }
+      if (iq == 0) {
+        const bool live = jt < nt;
+        st4(oRing + ((jt % (D + 1)) * H + ir) * 4,
+            make_float4(live ? S.s0.x : 0.f, live ? S.s1.x : 0.f, live ? S.s2.x : 0.f, 0.f));
+      }
+    };
+    auto la_load = [&](int jt, float (&lx)[32], float& ln0, float& ln1) {
+      ln0 = ln1 = 0.f;
+      if (jt < nt) {
+        const float* p = src + (long long)ir * W + jt * X + 32 * iq;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
+          lx[4 * q] = v.x;
+          lx[4 * q + 1] = v.y;
+          lx[4 * q + 2] = v.z;
+          lx[4 * q + 3] = v.w;
+        }
+        if (iq == TPR - 1 && jt + 1 < nt) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(p + 32));
+          ln0 = v.x;
+          ln1 = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) lx[q] = 0.f;
+      }
+    };
+
+    // ---- prologue ----
+    if (tid < H) {
+      const int je = min(nt, jst + (IIR ? D + 1 : 0) + g.P + 1);
+      prefetch_l2(src + (long long)tid * W + jst * X, (unsigned)((je - jst) * X * 4));
+    }
+    land(oF0, jst);
+    float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
+    if (IIR) {
+      for (int i = 1; i <= D; ++i) {
+        float lx[32], ln0, ln1;
+        la_load(jst + i, lx, ln0, ln1);
+        la_finish(jst + i, lx, ln0, ln1);
+      }
+    }
+
+    for (int j = jst; j < nt; ++j) {
+      const int cur = (j - jst) & 1;
+      const int oFc = cur ? oF1 : oF0;
+      const int oFp = cur ? oF0 : oF1;
+      if (tid < H) {
+        const int jp = j + (IIR ? D + 1 : 0) + g.P + 1;
+        if (jp < nt) prefetch_l2(src + (long long)tid * W + jp * X, (unsigned)(X * 4));
+      }
+      float lx[32], ln0 = 0.f, ln1 = 0.f;
+      const int jl = j + D + 1;
+      if (IIR) la_load(jl, lx, ln0, ln1);
+
+      cp_wait<0>();
+      __syncthreads();
+
+      if (IIR) {
+        // ---- local sweeps of this thread's chunk ----
+        const int rowF = oFc + ir * PF + HF + 32 * iq;
+        float x[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = ld4(rowF + 4 * q);
+          x[4 * q] = v.x;
+          x[4 * q + 1] = v.y;
+          x[4 * q + 2] = v.z;
+          x[4 * q + 3] = v.w;
+        }
+        const float4 vl = ld4(rowF - 4);
+        const float4 vr = ld4(rowF + 32);
+        float2 yp[32];
+        chunk_sweep<BETA>(x, vl.w, vl.z, vr.x, vr.y, k, yp);
+        // anticausal carry into this tile's right edge (Horner over the ring)
+        float tm[3];
+        {
+          const float4 a = ld4(oRing + (((j + D) % (D + 1)) * H + ir) * 4);
+          tm[0] = a.x;
+          tm[1] = a.y;
+          tm[2] = a.z;
+          for (int i = D - 1; i >= 1; --i) {
+            const float4 c = ld4(oRing + (((j + i) % (D + 1)) * H + ir) * 4);
+            float acc[3] = {c.x, c.y, c.z};
+            mv1(k.MX, tm, acc);
+            tm[0] = acc[0];
+            tm[1] = acc[1];
+            tm[2] = acc[2];
+          }
+        }
+        // ---- carries: inclusive scan over the row's chunks (causal up, anticausal down)
+        P3 S;
+        S.s0 = make_float2(yp[31].x, yp[31].y);
+        S.s1 = make_float2(yp[30].x, yp[30].y);
+        S.s2 = make_float2(yp[29].x, yp[29].y);
+        {
+          P3 E;
+          E.s0 = make_float2(cin0, tm[0]);
+          E.s1 = make_float2(cin1, tm[1]);
+          E.s2 = make_float2(cin2, tm[2]);
+          const P3 ME = mv(k.M1, E);
+          if (iq == 0) {
+            S.s0.x += ME.s0.x;
+            S.s1.x += ME.s1.x;
+            S.s2.x += ME.s2.x;
+          }
+          if (iq == TPR - 1) {
+            S.s0.y += ME.s0.y;
+            S.s1.y += ME.s1.y;
+            S.s2.y += ME.s2.y;
+          }
+        }
+#pragma unroll
+        for (int st = 0; (1 << st) < TPR; ++st) {
+          const int off = 8 << st;
+          P3 o;
+          o.s0 = make_float2(__shfl_up_sync(0xffffffffu, S.s0.x, off), __shfl_down_sync(0xffffffffu, S.s0.y, off));
+          o.s1 = make_float2(__shfl_up_sync(0xffffffffu, S.s1.x, off), __shfl_down_sync(0xffffffffu, S.s1.y, off));
+          o.s2 = make_float2(__shfl_up_sync(0xffffffffu, S.s2.x, off), __shfl_down_sync(0xffffffffu, S.s2.y, off));
+          const P3 t = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
+          if (iq >= (1 << st)) {
+            S.s0.x += t.s0.x;
+            S.s1.x += t.s1.x;
+            S.s2.x += t.s2.x;
+          }
+          if (iq + (1 << st) < TPR) {
+            S.s0.y += t.s0.y;
+            S.s1.y += t.s1.y;
+            S.s2.y += t.s2.y;
+          }
+        }
+        // exclusive carries of this chunk
+        P3 cc;
+        {
+          const float u0 = __shfl_up_sync(0xffffffffu, S.s0.x, 8);
+          const float u1 = __shfl_up_sync(0xffffffffu, S.s1.x, 8);
+          const float u2 = __shfl_up_sync(0xffffffffu, S.s2.x, 8);
+          const float d0 = __shfl_down_sync(0xffffffffu, S.s0.y, 8);
+          const float d1 = __shfl_down_sync(0xffffffffu, S.s1.y, 8);
+          const float d2 = __shfl_down_sync(0xffffffffu, S.s2.y, 8);
+          cc.s0 = make_float2(iq == 0 ? cin0 : u0, iq == TPR - 1 ? tm[0] : d0);
+          cc.s1 = make_float2(iq == 0 ? cin1 : u1, iq == TPR - 1 ? tm[1] : d1);
+          cc.s2 = make_float2(iq == 0 ? cin2 : u2, iq == TPR - 1 ? tm[2] : d2);
+        }
+        // causal carry for the next tile: inclusive state of the row's last chunk
+        {
+          const int srcl = (lane & 7) | (8 * (TPR - 1)) | (lane & ~(8 * TPR - 1));
+          cin0 = __shfl_sync(0xffffffffu, S.s0.x, srcl);
+          cin1 = __shfl_sync(0xffffffffu, S.s1.x, srcl);
+          cin2 = __shfl_sync(0xffffffffu, S.s2.x, srcl);
+        }
+        // ---- fix-up with the homogeneous responses ----
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float2 v = yp[i];
+          v = __ffma2_rn(k.G[i][0], cc.s0, v);
+          v = __ffma2_rn(k.G[i][1], cc.s1, v);
+          v = __ffma2_rn(k.G[i][2], cc.s2, v);
+          yp[i] = v;
+        }
+        __syncthreads();   // every raw read of this tile is done
+        // halo: previous tile's last HF filtered columns (zero before the first tile)
+        for (int e = tid; e < 2 * H; e += NT) {
+          const int r = e >> 1, qd = e & 1;
+          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + r * PF + X + 4 * qd);
+          st4(oFc + r * PF + 4 * qd, h);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int i = 4 * q;
+          st4(rowF + i, make_float4(yp[i].x + yp[31 - i].y, yp[i + 1].x + yp[30 - i].y,
+                                    yp[i + 2].x + yp[29 - i].y, yp[i + 3].x + yp[28 - i].y));
+        }
+      } else {
+        for (int e = tid; e < 2 * H; e += NT) {
+          const int r = e >> 1, qd = e & 1;
+          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + r * PF + X + 4 * qd);
+          st4(oFc + r * PF + 4 * qd, h);
+        }
+      }
+      __syncthreads();                                   // F tile complete
+      if (j + 1 < nt) land(oFp, j + 1);
+
+      // ---- FHT step 1 (levels 1-3): F -> S1 ----
+      if (j >= j0) {
+        constexpr int NCH = X / C1;
+        const int jj = tid % NCH, G = tid / NCH;
+        float v[8][It<3, C1>::T];
+        item_load<3, C1>(oFc + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
+        item_fht<3, C1>(v);
+        const int gb = G & (NR2 - 1);                   // next step's block index
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int o = oS + (G * 8 + r) * PS + HS + C1 * jj + ((r * gb) & 3);
+#pragma unroll
+          for (int t = 0; t < C1; ++t) sm[o + t] = v[r][It<3, C1>::O + t];
+        }
+      }
+      __syncthreads();
+      // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
+      if (j >= j0) {
+        constexpr int NCH = X / C2;
+        const int jj = tid % NCH, c = tid / NCH;
+        float v[NR2][It<R2, C2>::T];
+        item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
+        item_fht<R2, C2>(v);
+        const int ubase = j * X + C2 * jj;
+#pragma unroll
+        for (int r = 0; r < NR2; ++r) {
+          const int cf = c * NR2 + r;
+          const int ulo = N - b * (cf + 1);
+          const int uhi = W - cf * b;
+          float* o = dstR + (long long)cf * WR + (cf * b - N + NB);
+          if (ubase >= ulo && ubase + C2 <= uhi) {
+#pragma unroll
+            for (int t = 0; t < C2; ++t) o[ubase + t] = v[r][O2 + t];
+          } else if (ubase + C2 > ulo && ubase < uhi) {
+#pragma unroll
+            for (int t = 0; t < C2; ++t) {
+              const int u = ubase + t;
+              if (u >= ulo && u < uhi) o[u] = v[r][O2 + t];
+            }
+          }
+        }
+      }
+      if (IIR) la_finish(jl, lx, ln0, ln1);
+      __syncthreads();
+      // ---- S1 halo for the next tile ----
+      if (j >= j0) {
+        constexpr int NQ = (HS + 4) / 4;
+        for (int e = tid; e < H * NQ; e += NT) {
+          const int r = e / NQ, qd = e - r * NQ;
+          st4(oS + r * PS + 4 * qd, ld4(oS + r * PS + X + 4 * qd));
+        }
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// Pass B, one family pair (Eq.22): CTA item = (slice, pass-A channel ch, x-tile).
+// Family 2p (q = 0) at x0, family 2p+1 (q = 1) at the mirrored tile N - x0 - XB.
+// Input rows b of G_ch[b][v] = R_A[b][ch][v - ch*b] (compact layout; the
+// pre-shift is addressing).  Step 1 (R1 levels) over [core - HS, core + XB),
+// step 2 (R2 levels) over the core, outputs parked, then the pair epilogue.
+// ===========================================================================
+template <int R1, int R2, int XB>
+__global__ void __launch_bounds__(256, 1)
+    k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, int slices,
+             int pair, float scale, long long nitems) {
+  constexpr int NT = 256;
+  constexpr int NB = 1 << (R1 + R2);
+  constexpr int NR1 = 1 << R1, NR2 = 1 << R2;
+  constexpr int C1 = (R1 == 3) ? 4 : 8;
+  constexpr int C2 = (R2 == 3) ? 4 : 8;
+  constexpr int O1 = It<R1, C1>::O, O2 = It<R2, C2>::O;
+  constexpr int HS = pb_halo(R1, R2);
+  constexpr int HI = HS + O1;
+  const int N = g.N, H = g.H, WR = g.WR;
+  constexpr int PI = pitch4(HI + XB);
+  constexpr int PS = pitch4(HS + XB + 4);
+  constexpr int PK = XB + 4;
+  constexpr int oIn = 0;                               // [2 buf][2 fam][NB][PI]
+  constexpr int oS = 4 * NB * PI;                      // [2 fam][NB][PS]
+  constexpr int oK = oS + 2 * NB * PS;                 // [2 fam][NB][PK]
+  static_assert((HS + XB) % C1 == 0 && XB % C2 == 0, "pass-B item tiling");
+  const int tid = threadIdx.x;
+  const int nx = (N + XB - 1) / XB;
+
+  auto decode = [&](long long t, long long& sl, int& ch, int& x0) {
+    const long long per = (long long)nx * H;
+    sl = t / per;
+    const int rem = (int)(t - sl * per);
+    ch = rem / nx;
+    x0 = (rem - ch * nx) * XB;
+  };
+  auto fill = [&](int buf, long long t) {
+    long long sl;
+    int ch, x0;
+    decode(t, sl, ch, x0);
+    constexpr int nq = (HI + XB) / 4;
+    for (int e = tid; e < 2 * NB * nq; e += NT) {
+      const int q = e / (NB * nq);
+      const int rem = e - q * NB * nq;
+      const int bq = rem / nq, qd = rem - bq * nq;
+      const int xs = (q == 0) ? x0 : (N - x0 - XB);
+      const int jp = xs - HI + NB + 4 * qd;            // compact column j' = v - N + NB
+      const float* row = Rin + ((((sl * 4 + 2 * pair + q) * NB + bq) * (long long)H) + ch) * WR;
+      const bool ok = (jp >= 0) && (jp < WR);
+      cp16(oIn + ((buf * 2 + q) * NB + bq) * PI + 4 * qd, ok ? row + jp : row, ok);
+    }
+    cp_commit();
+  };
+
+  long long t = blockIdx.x;
+  if (t >= nitems) return;
+  fill(0, t);
+  int buf = 0;
+  while (true) {
+    const long long tn = t + gridDim.x;
+    long long sl;
+    int ch, x0;
+    decode(t, sl, ch, x0);
+    cp_wait<0>();
+    __syncthreads();
+    // ---- step 1: both families, output virtual cols [0, HS + XB) ----
+    {
+      constexpr int nch = (HS + XB) / C1;
+      constexpr int per_fam = (NB / NR1) * nch;
+      for (int it = tid; it < 2 * per_fam; it += NT) {
+        const int q = it / per_fam;
+        const int rem = it - q * per_fam;
+        const int G = rem / nch, jj = rem - G * nch;
+        float v[NR1][It<R1, C1>::T];
+        item_load<R1, C1>(oIn + ((buf * 2 + q) * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
+        item_fht<R1, C1>(v);
+#pragma unroll
+        for (int r = 0; r < NR1; ++r) {
+          const int o = oS + (q * NB + G * NR1 + r) * PS + C1 * jj + ((r * G) & 3);
+#pragma unroll
+          for (int tt = 0; tt < C1; ++tt) sm[o + tt] = v[r][O1 + tt];
+        }
+      }
+    }
+    __syncthreads();
+    if (tn < nitems) fill(buf ^ 1, tn);
+    // ---- step 2: both families, core columns -> park ----
+    {
+      constexpr int nch = XB / C2;
+      constexpr int per_fam = NR1 * nch;
+      for (int it = tid; it < 2 * per_fam; it += NT) {
+        const int q = it / per_fam;
+        const int rem = it - q * per_fam;
+        const int c = rem / nch, jj = rem - c * nch;
+        float v[NR2][It<R2, C2>::T];
+        item_load<R2, C2>(oS + (q * NB + c) * PS + HS + C2 * jj - O2, NR1 * PS, c, v);
+        item_fht<R2, C2>(v);
+#pragma unroll
+        for (int r = 0; r < NR2; ++r) {
+          const int o = oK + (q * NB + c * NR2 + r) * PK + C2 * jj;
+#pragma unroll
+          for (int tt = 0; tt < C2; tt += 4)
+            st4(o + tt, make_float4(v[r][O2 + tt], v[r][O2 + tt + 1], v[r][O2 + tt + 2], v[r][O2 + tt + 3]));
+        }
+      }
+    }
+    __syncthreads();
+    // ---- epilogue: Eq.22 pair, weight, store ----
+    float* out = img + sl * (long long)N * N;
+    if (pair == 0) {
+      constexpr int nq = XB / 4;
+      for (int e = tid; e < NB * nq; e += NT) {
+        const int rf = e / nq, kq = e - rf * nq;
+        const float4 a = ld4(oK + rf * PK + 4 * kq);
+        const float4 m = ld4(oK + (NB + rf) * PK + XB - 4 - 4 * kq);
+        const int x = x0 + 4 * kq;
+        if (x < N) {
+          float4 o = make_float4(scale * (a.x + m.w), scale * (a.y + m.z), scale * (a.z + m.y),
+                                 scale * (a.w + m.x));
+          *reinterpret_cast<float4*>(out + (long long)(ch * NB + rf) * N + x) = o;
+        }
+      }
+    } else {
+      // out[x0 + i][ch*NB + rf] += scale * (B2[rf][i] + B3[rf][XB-1-i]); one image row per lane
+      constexpr int halves = NT / XB > 0 ? NT / XB : 1;
+      for (int e = tid; e < XB * halves; e += NT) {
+        const int i = e % XB, hh = e / XB;
+        const int x = x0 + i;
+        if (x >= N) continue;
+        const int r0 = hh * (NB / halves), r1 = r0 + NB / halves;
+        float* orow = out + (long long)x * N + ch * NB;
+        for (int rf = r0; rf < r1; rf += 4) {
+          float4 o = *reinterpret_cast<float4*>(orow + rf);
+          o.x += scale * (sm[oK + rf * PK + i] + sm[oK + (NB + rf) * PK + XB - 1 - i]);
+          o.y += scale * (sm[oK + (rf + 1) * PK + i] + sm[oK + (NB + rf + 1) * PK + XB - 1 - i]);
+          o.z += scale * (sm[oK + (rf + 2) * PK + i] + sm[oK + (NB + rf + 2) * PK + XB - 1 - i]);
+          o.w += scale * (sm[oK + (rf + 3) * PK + i] + sm[oK + (NB + rf + 3) * PK + XB - 1 - i]);
+          *reinterpret_cast<float4*>(orow + rf) = o;
+        }
+      }
+    }
+    if (tn >= nitems) break;
+    t = tn;
+    buf ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+bool sweep_supported(int N) { return N == 512 || N == 1024 || N == 2048; }
+
+size_t sweep_a_smem(const SweepGeom& g) {
+  const int H = g.H, X = g.X;
+  const int R2 = (H == 64) ? 3 : 2;
+  const int O2 = 4;
+  const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : O2 + 4 * ((7 * 3) / 4);
+  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
+  return ((size_t)2 * H * PF + (size_t)H * PS + (size_t)(g.D + 1) * H * 4 + 4) * sizeof(float);
+}
+
+size_t pair_b_smem(const SweepGeom& g) {
+  const int NB = g.NB, XB = g.XB;
+  int m = 0;
+  while ((1 << m) < NB) ++m;
+  const int R1 = (m >= 5) ? 3 : 2, R2 = m - R1;
+  const int O1 = (R1 == 3) ? 8 : 4;
+  const int HS = pb_halo(R1, R2);
+  const int HI = HS + O1;
+  const int PI = pitch4(HI + XB), PS = pitch4(HS + XB + 4), PK = XB + 4;
+  return ((size_t)4 * NB * PI + (size_t)2 * NB * PS + (size_t)2 * NB * PK) * sizeof(float);
+}
+
+template <int H, int X, bool IIR, bool BETA>
+static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, int nf,
+                              long long stride, const SweepGeom& g, const SweepIir& k, int* counter,
+                              cudaStream_t st) {
+  auto kern = k_sweep_a<H, X, IIR, BETA>;
+  const size_t smem = sweep_a_smem(g);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, H * X / 32, smem);
+  if (per < 1) per = 1;
+  const long long nitems = (long long)slices * nf * g.NB;
+  const long long grid = std::min<long long>(nitems, (long long)sms * per);
+  e = cudaMemsetAsync(counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, counter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int nf,
+                           long long lin_slice_stride, const SweepGeom& g, const SweepIir& k,
+                           bool iir, int* counter, cudaStream_t st, int* launches) {
+  if (slices <= 0 || nf <= 0) return cudaSuccess;
+  const bool beta = k.beta.x != 0.0f;
+  cudaError_t e;
+#define FBP_SWEEP_CASE(HH, XX)                                                                     \
+  if (g.H == HH) {                                                                                 \
+    if (!iir) e = launch_a_t<HH, XX, false, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
+    else if (beta) e = launch_a_t<HH, XX, true, true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
+    else e = launch_a_t<HH, XX, true, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
+    if (launches) ++*launches;                                                                     \
+    return e;                                                                                      \
+  }
+  FBP_SWEEP_CASE(64, 64)
+  FBP_SWEEP_CASE(32, 128)
+#undef FBP_SWEEP_CASE
+  return cudaErrorInvalidValue;
+}
+
+template <int R1, int R2, int XB>
+static cudaError_t launch_b_t(const float* R, float* img, int slices, int pair, float scale,
+                              const SweepGeom& g, cudaStream_t st) {
+  auto kern = k_pair_b<R1, R2, XB>;
+  const size_t smem = pair_b_smem(g);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem);
+  if (per < 1) per = 1;
+  const long long nitems = (long long)((g.N + g.XB - 1) / g.XB) * g.H * slices;
+  const long long grid = std::min<long long>(nitems, (long long)sms * per);
+  kern<<<(unsigned)grid, 256, smem, st>>>(R, img, g, slices, pair, scale, nitems);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, float scale,
+                          const SweepGeom& g, cudaStream_t st, int* launches) {
+  if (slices <= 0) return cudaSuccess;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (g.XB != 128) return cudaErrorInvalidValue;
+  if (g.NB == 16) e = launch_b_t<2, 2, 128>(R, img, slices, pair, scale, g, st);
+  else if (g.NB == 32) e = launch_b_t<3, 2, 128>(R, img, slices, pair, scale, g, st);
+  if (launches) ++*launches;
+  return e;
+}
+
+}  // namespace fbp

@@ -25,7 +25,8 @@ FBP_STATUS = {0: "FBP_OK", 1: "FBP_ERR_PLAN", 2: "FBP_ERR_PARAM", 3: "FBP_ERR_UN
 
 EXPORTED = ["fbp_plan_create", "fbp_plan_destroy", "fbp_iir_filter", "fbp_fht_backproject",
             "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
-            "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_profile", "fbp_plan_kernel_times"]
+            "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_path", "fbp_plan_profile",
+            "fbp_plan_kernel_times"]
 
 KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b")
 
@@ -65,6 +66,8 @@ def lib():
     L.fbp_plan_launch_count.restype = ctypes.c_longlong
     L.fbp_plan_info.argtypes = [vp] + [ctypes.POINTER(i)] * 4 + [ctypes.POINTER(ctypes.c_longlong)]
     L.fbp_plan_info.restype = i
+    L.fbp_plan_path.argtypes = [vp] + [ctypes.POINTER(i)] * 3
+    L.fbp_plan_path.restype = i
     L.fbp_plan_profile.argtypes = [vp, i]
     L.fbp_plan_profile.restype = i
     L.fbp_plan_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double),
@@ -119,6 +122,12 @@ class Plan:
         _check(lib().fbp_plan_info(self._h, ctypes.byref(n), ctypes.byref(k1), ctypes.byref(m),
                                    ctypes.byref(grp), ctypes.byref(ws)))
         return dict(N=n.value, k1=k1.value, m=m.value, group=grp.value, workspace_bytes=ws.value)
+
+    def path(self) -> dict:
+        """Schedule: fused sweep fast path or the separate-kernel path (fbp_plan_path)."""
+        fast, d, x = (ctypes.c_int() for _ in range(3))
+        _check(lib().fbp_plan_path(self._h, ctypes.byref(fast), ctypes.byref(d), ctypes.byref(x)))
+        return dict(fast=bool(fast.value), lookahead_tiles=d.value, tile_width=x.value)
 
     def launch_count(self) -> int:
         """Kernels launched by the last call on this plan."""
