@@ -53,8 +53,8 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int NLEFT>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
 
-__device__ __forceinline__ void prefetch_l2(const float* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ void prefetch_line(const float* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 // Row pitch (floats) for a row of at least w floats: a multiple of 4 whose quad
@@ -172,17 +172,19 @@ __device__ __forceinline__ void mv1(const float2 (&M)[9], const float (&v)[3], f
 template <bool BETA>
 __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, float xl1, float xr0,
                                             float xr1, const SweepIir& k, float2 (&yp)[32]) {
-  const float2 m1 = make_float2(-1.0f, -1.0f);
-  float2 xprev = make_float2(xl0, xr0);
   float2 dprev = make_float2(xl0 - xl1, xr0 - xr1);
   float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    const float2 xx = make_float2(x[i], x[31 - i]);
-    const float2 d = __ffma2_rn(m1, xprev, xx);
+    float2 d;
+    d.x = x[i] - (i == 0 ? xl0 : x[i - 1]);
+    d.y = x[31 - i] - (i == 0 ? xr0 : x[32 - i]);
     float2 u = __fmul2_rn(k.c1, dprev);
     u = __ffma2_rn(k.c0, d, u);
-    if (BETA) u = __ffma2_rn(k.beta, xx, u);
+    if (BETA) {
+      u.x = fmaf(k.beta.x, x[i], u.x);
+      u.y = fmaf(k.beta.x, x[31 - i], u.y);
+    }
     float2 v = __ffma2_rn(k.na3, y3, u);
     v = __ffma2_rn(k.na2, y2, v);
     v = __ffma2_rn(k.na1, y1, v);
@@ -190,7 +192,6 @@ __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, flo
     y2 = y1;
     y1 = v;
     dprev = d;
-    xprev = xx;
     yp[i] = v;
   }
 }
@@ -201,17 +202,19 @@ __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, flo
 template <bool BETA>
 __device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], float xn0, float xn1,
                                                        const SweepIir& k, float (&va)[3]) {
-  const float2 m1 = make_float2(-1.0f, -1.0f);
-  float2 xprev = make_float2(x[16], xn0);
   float2 dprev = make_float2(x[16] - x[17], xn0 - xn1);
   float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    const float2 xx = make_float2(x[15 - i], x[31 - i]);
-    const float2 d = __ffma2_rn(m1, xprev, xx);
+    float2 d;
+    d.x = x[15 - i] - x[16 - i];
+    d.y = x[31 - i] - (i == 0 ? xn0 : x[32 - i]);
     float2 u = __fmul2_rn(k.c1, dprev);
     u = __ffma2_rn(k.c0, d, u);
-    if (BETA) u = __ffma2_rn(k.beta, xx, u);
+    if (BETA) {
+      u.x = fmaf(k.beta.x, x[15 - i], u.x);
+      u.y = fmaf(k.beta.x, x[31 - i], u.y);
+    }
     float2 v = __ffma2_rn(k.na3, y3, u);
     v = __ffma2_rn(k.na2, y2, v);
     v = __ffma2_rn(k.na1, y1, v);
@@ -219,7 +222,6 @@ __device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], flo
     y2 = y1;
     y1 = v;
     dprev = d;
-    xprev = xx;
   }
   const float hi[3] = {y1.y, y2.y, y3.y};
   va[0] = y1.x;
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(H * X / 32)
     };
 
     // look-ahead: anticausal aggregate of tile jt from registers -> ring
-    auto la_finish = [&](int jt, const float (&lx)[32], float ln0, float ln1) {
+    auto la_finish = [&](int jt, int slot, const float (&lx)[32], float ln0, float ln1) {
       float va[3];
       // right neighbours of this chunk: next chunk's first two samples (or next tile's)
       const float p0 = __shfl_down_sync(0xffffffffu, lx[0], 8);
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(H * X / 32)
       }
       if (iq == 0) {
         const bool live = jt < nt;
-        st4(oRing + ((jt % (D + 1)) * H + ir) * 4,
+        st4(oRing + (slot * H + ir) * 4,
             make_float4(live ? S.s0.x : 0.f, live ? S.s1.x : 0.f, live ? S.s2.x : 0.f, 0.f));
       }
     };
@@ -365,9 +367,14 @@ __global__ void __launch_bounds__(H * X / 32)
     };
 
     // ---- prologue ----
-    if (tid < H) {
+    {
+      // L2 prefetch of the sweep's first tiles (one 128-byte line per thread per step)
       const int je = min(nt, jst + (IIR ? D + 1 : 0) + g.P + 1);
-      prefetch_l2(src + (long long)tid * W + jst * X, (unsigned)((je - jst) * X * 4));
+      constexpr int LPR = X / 32;                       // lines per row per tile
+      for (int e = tid; e < H * LPR * (je - jst); e += NT) {
+        const int r = e % H, rest = e / H;
+        prefetch_line(src + (long long)r * W + jst * X + 32 * rest);
+      }
     }
     land(oF0, jst);
     float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
@@ -375,17 +382,20 @@ __global__ void __launch_bounds__(H * X / 32)
       for (int i = 1; i <= D; ++i) {
         float lx[32], ln0, ln1;
         la_load(jst + i, lx, ln0, ln1);
-        la_finish(jst + i, lx, ln0, ln1);
+        la_finish(jst + i, i, lx, ln0, ln1);       // tile jst + i -> slot i
       }
     }
+    int slot_j = 0;                                    // ring slot of tile j (j - jst mod D+1)
 
     for (int j = jst; j < nt; ++j) {
       const int cur = (j - jst) & 1;
       const int oFc = cur ? oF1 : oF0;
       const int oFp = cur ? oF0 : oF1;
-      if (tid < H) {
+      {
         const int jp = j + (IIR ? D + 1 : 0) + g.P + 1;
-        if (jp < nt) prefetch_l2(src + (long long)tid * W + jp * X, (unsigned)(X * 4));
+        constexpr int LPR = X / 32;
+        if (jp < nt && tid < H * LPR)
+          prefetch_line(src + (long long)(tid % H) * W + jp * X + 32 * (tid / H));
       }
       float lx[32], ln0 = 0.f, ln1 = 0.f;
       const int jl = j + D + 1;
@@ -413,12 +423,15 @@ __global__ void __launch_bounds__(H * X / 32)
         // anticausal carry into this tile's right edge (Horner over the ring)
         float tm[3];
         {
-          const float4 a = ld4(oRing + (((j + D) % (D + 1)) * H + ir) * 4);
+          int sl = slot_j + D;                             // slot of tile j + D
+          if (sl > D) sl -= D + 1;
+          const float4 a = ld4(oRing + (sl * H + ir) * 4);
           tm[0] = a.x;
           tm[1] = a.y;
           tm[2] = a.z;
           for (int i = D - 1; i >= 1; --i) {
-            const float4 c = ld4(oRing + (((j + i) % (D + 1)) * H + ir) * 4);
+            sl = (sl == 0) ? D : sl - 1;                     // slot of tile j + i
+            const float4 c = ld4(oRing + (sl * H + ir) * 4);
             float acc[3] = {c.x, c.y, c.z};
             mv1(k.MX, tm, acc);
             tm[0] = acc[0];
@@ -487,14 +500,20 @@ __global__ void __launch_bounds__(H * X / 32)
           cin1 = __shfl_sync(0xffffffffu, S.s1.x, srcl);
           cin2 = __shfl_sync(0xffffffffu, S.s2.x, srcl);
         }
-        // ---- fix-up with the homogeneous responses ----
+        // ---- fix-up: add the homogeneous response to the carry-in state, run as the
+        //      zero-input recursion from (cc) -- h_i = (A^(i+1) cc)_0, packed ----
+        {
+          float2 h1 = cc.s0, h2 = cc.s1, h3 = cc.s2;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float2 v = yp[i];
-          v = __ffma2_rn(k.G[i][0], cc.s0, v);
-          v = __ffma2_rn(k.G[i][1], cc.s1, v);
-          v = __ffma2_rn(k.G[i][2], cc.s2, v);
-          yp[i] = v;
+          for (int i = 0; i < 32; ++i) {
+            float2 h = __fmul2_rn(k.na3, h3);
+            h = __ffma2_rn(k.na2, h2, h);
+            h = __ffma2_rn(k.na1, h1, h);
+            h3 = h2;
+            h2 = h1;
+            h1 = h;
+            yp[i] = __fadd2_rn(yp[i], h);
+          }
         }
         __syncthreads();   // every raw read of this tile is done
         // halo: previous tile's last HF filtered columns (zero before the first tile)
@@ -561,7 +580,8 @@ __global__ void __launch_bounds__(H * X / 32)
           }
         }
       }
-      if (IIR) la_finish(jl, lx, ln0, ln1);
+      if (IIR) la_finish(jl, slot_j, lx, ln0, ln1);   // tile j + D + 1 reuses tile j's slot
+      slot_j = (slot_j == D) ? 0 : slot_j + 1;
       __syncthreads();
       // ---- S1 halo for the next tile ----
       if (j >= j0) {
@@ -580,12 +600,17 @@ __global__ void __launch_bounds__(H * X / 32)
 // Family 2p (q = 0) at x0, family 2p+1 (q = 1) at the mirrored tile N - x0 - XB.
 // Input rows b of G_ch[b][v] = R_A[b][ch][v - ch*b] (compact layout; the
 // pre-shift is addressing).  Step 1 (R1 levels) over [core - HS, core + XB),
-// step 2 (R2 levels) over the core, outputs parked, then the pair epilogue.
+// step 2 (R2 levels) over the core; the final rows are parked (aliasing the
+// input buffer) and the pair epilogue mirrors, adds, weights and stores:
+//   PAIR 0:  img[ch*NB + r][x0 + i]  = w (B0[r][i] + B1[r][XB-1-i])
+//   PAIR 1:  img[x0 + i][ch*NB + r] += w (B2[r][i] + B3[r][XB-1-i])
+// For PAIR 1 the image rows are staged into shared memory by cp.async while
+// the FHT steps run.  Two CTAs per SM; no cross-item prefetch.
 // ===========================================================================
-template <int R1, int R2, int XB>
-__global__ void __launch_bounds__(256, 1)
-    k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, int slices,
-             int pair, float scale, long long nitems) {
+template <int R1, int R2, int XB, int PAIR>
+__global__ void __launch_bounds__(256, 2)
+    k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
+             long long nitems) {
   constexpr int NT = 256;
   constexpr int NB = 1 << (R1 + R2);
   constexpr int NR1 = 1 << R1, NR2 = 1 << R2;
@@ -594,51 +619,50 @@ __global__ void __launch_bounds__(256, 1)
   constexpr int O1 = It<R1, C1>::O, O2 = It<R2, C2>::O;
   constexpr int HS = pb_halo(R1, R2);
   constexpr int HI = HS + O1;
-  const int N = g.N, H = g.H, WR = g.WR;
   constexpr int PI = pitch4(HI + XB);
   constexpr int PS = pitch4(HS + XB + 4);
-  constexpr int PK = XB + 4;
-  constexpr int oIn = 0;                               // [2 buf][2 fam][NB][PI]
-  constexpr int oS = 4 * NB * PI;                      // [2 fam][NB][PS]
-  constexpr int oK = oS + 2 * NB * PS;                 // [2 fam][NB][PK]
+  constexpr int PK = PAIR == 0 ? XB + 4 : XB + 1;     // pair 1 reads park columns
+  constexpr int PG = NB + 4;                          // image staging pitch (pair 1)
+  constexpr int oIn = 0;                              // [2 fam][NB][PI]; park aliases it
+  constexpr int oS = 2 * NB * PI;                     // [2 fam][NB][PS]
+  constexpr int oG = oS + 2 * NB * PS;                // [XB][PG] image rows (pair 1)
   static_assert((HS + XB) % C1 == 0 && XB % C2 == 0, "pass-B item tiling");
+  static_assert(2 * NB * PK <= 2 * NB * PI, "park must fit in the input buffer");
+  const int N = g.N, H = g.H, WR = g.WR;
   const int tid = threadIdx.x;
   const int nx = (N + XB - 1) / XB;
 
-  auto decode = [&](long long t, long long& sl, int& ch, int& x0) {
+  for (long long t = blockIdx.x; t < nitems; t += gridDim.x) {
     const long long per = (long long)nx * H;
-    sl = t / per;
+    const long long sl = t / per;
     const int rem = (int)(t - sl * per);
-    ch = rem / nx;
-    x0 = (rem - ch * nx) * XB;
-  };
-  auto fill = [&](int buf, long long t) {
-    long long sl;
-    int ch, x0;
-    decode(t, sl, ch, x0);
-    constexpr int nq = (HI + XB) / 4;
-    for (int e = tid; e < 2 * NB * nq; e += NT) {
-      const int q = e / (NB * nq);
-      const int rem = e - q * NB * nq;
-      const int bq = rem / nq, qd = rem - bq * nq;
-      const int xs = (q == 0) ? x0 : (N - x0 - XB);
-      const int jp = xs - HI + NB + 4 * qd;            // compact column j' = v - N + NB
-      const float* row = Rin + ((((sl * 4 + 2 * pair + q) * NB + bq) * (long long)H) + ch) * WR;
-      const bool ok = (jp >= 0) && (jp < WR);
-      cp16(oIn + ((buf * 2 + q) * NB + bq) * PI + 4 * qd, ok ? row + jp : row, ok);
+    const int ch = rem / nx;
+    const int x0 = (rem - ch * nx) * XB;
+    float* out = img + sl * (long long)N * N;
+    // ---- fills: both families' compact rows (+ image rows for pair 1) ----
+    {
+      constexpr int nq = (HI + XB) / 4;
+      for (int e = tid; e < 2 * NB * nq; e += NT) {
+        const int q = e / (NB * nq);
+        const int r2 = e - q * NB * nq;
+        const int bq = r2 / nq, qd = r2 - bq * nq;
+        const int xs = (q == 0) ? x0 : (N - x0 - XB);
+        const int jp = xs - HI + NB + 4 * qd;         // compact column j' = v - N + NB
+        const float* row = Rin + ((((sl * 4 + 2 * PAIR + q) * NB + bq) * (long long)H) + ch) * WR;
+        const bool ok = (jp >= 0) && (jp < WR);
+        cp16(oIn + (q * NB + bq) * PI + 4 * qd, ok ? row + jp : row, ok);
+      }
+      if (PAIR == 1) {
+        constexpr int gq = NB / 4;
+        for (int e = tid; e < XB * gq; e += NT) {
+          const int i = e / gq, qd = e - i * gq;
+          const bool ok = x0 + i < N;
+          const float* src = out + (long long)(ok ? x0 + i : 0) * N + ch * NB + 4 * qd;
+          cp16(oG + i * PG + 4 * qd, src, ok);
+        }
+      }
+      cp_commit();
     }
-    cp_commit();
-  };
-
-  long long t = blockIdx.x;
-  if (t >= nitems) return;
-  fill(0, t);
-  int buf = 0;
-  while (true) {
-    const long long tn = t + gridDim.x;
-    long long sl;
-    int ch, x0;
-    decode(t, sl, ch, x0);
     cp_wait<0>();
     __syncthreads();
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
@@ -647,10 +671,10 @@ __global__ void __launch_bounds__(256, 1)
       constexpr int per_fam = (NB / NR1) * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
         const int q = it / per_fam;
-        const int rem = it - q * per_fam;
-        const int G = rem / nch, jj = rem - G * nch;
+        const int r3 = it - q * per_fam;
+        const int G = r3 / nch, jj = r3 - G * nch;
         float v[NR1][It<R1, C1>::T];
-        item_load<R1, C1>(oIn + ((buf * 2 + q) * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
+        item_load<R1, C1>(oIn + (q * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
         item_fht<R1, C1>(v);
 #pragma unroll
         for (int r = 0; r < NR1; ++r) {
@@ -661,65 +685,63 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     __syncthreads();
-    if (tn < nitems) fill(buf ^ 1, tn);
-    // ---- step 2: both families, core columns -> park ----
+    // ---- step 2: both families, core columns -> park (aliasing the input) ----
     {
       constexpr int nch = XB / C2;
       constexpr int per_fam = NR1 * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
         const int q = it / per_fam;
-        const int rem = it - q * per_fam;
-        const int c = rem / nch, jj = rem - c * nch;
+        const int r3 = it - q * per_fam;
+        const int c = r3 / nch, jj = r3 - c * nch;
         float v[NR2][It<R2, C2>::T];
         item_load<R2, C2>(oS + (q * NB + c) * PS + HS + C2 * jj - O2, NR1 * PS, c, v);
         item_fht<R2, C2>(v);
 #pragma unroll
         for (int r = 0; r < NR2; ++r) {
-          const int o = oK + (q * NB + c * NR2 + r) * PK + C2 * jj;
+          const int o = oIn + (q * NB + c * NR2 + r) * PK + C2 * jj;
+          if (PAIR == 0) {
 #pragma unroll
-          for (int tt = 0; tt < C2; tt += 4)
-            st4(o + tt, make_float4(v[r][O2 + tt], v[r][O2 + tt + 1], v[r][O2 + tt + 2], v[r][O2 + tt + 3]));
+            for (int tt = 0; tt < C2; tt += 4)
+              st4(o + tt, make_float4(v[r][O2 + tt], v[r][O2 + tt + 1], v[r][O2 + tt + 2], v[r][O2 + tt + 3]));
+          } else {
+#pragma unroll
+            for (int tt = 0; tt < C2; ++tt) sm[o + tt] = v[r][O2 + tt];
+          }
         }
       }
     }
     __syncthreads();
-    // ---- epilogue: Eq.22 pair, weight, store ----
-    float* out = img + sl * (long long)N * N;
-    if (pair == 0) {
+    // ---- epilogue ----
+    if (PAIR == 0) {
       constexpr int nq = XB / 4;
       for (int e = tid; e < NB * nq; e += NT) {
         const int rf = e / nq, kq = e - rf * nq;
-        const float4 a = ld4(oK + rf * PK + 4 * kq);
-        const float4 m = ld4(oK + (NB + rf) * PK + XB - 4 - 4 * kq);
+        const float4 a = ld4(oIn + rf * PK + 4 * kq);
+        const float4 m = ld4(oIn + (NB + rf) * PK + XB - 4 - 4 * kq);
         const int x = x0 + 4 * kq;
         if (x < N) {
-          float4 o = make_float4(scale * (a.x + m.w), scale * (a.y + m.z), scale * (a.z + m.y),
-                                 scale * (a.w + m.x));
+          const float4 o = make_float4(scale * (a.x + m.w), scale * (a.y + m.z), scale * (a.z + m.y),
+                                       scale * (a.w + m.x));
           *reinterpret_cast<float4*>(out + (long long)(ch * NB + rf) * N + x) = o;
         }
       }
     } else {
-      // out[x0 + i][ch*NB + rf] += scale * (B2[rf][i] + B3[rf][XB-1-i]); one image row per lane
-      constexpr int halves = NT / XB > 0 ? NT / XB : 1;
-      for (int e = tid; e < XB * halves; e += NT) {
-        const int i = e % XB, hh = e / XB;
+      // lanes: 8 row-quads of one image row x 4 image rows per warp (coalesced 128 B rows)
+      constexpr int gq = NB / 4;
+      for (int e = tid; e < XB * gq; e += NT) {
+        const int i = e / gq, rq = e - i * gq;
         const int x = x0 + i;
         if (x >= N) continue;
-        const int r0 = hh * (NB / halves), r1 = r0 + NB / halves;
-        float* orow = out + (long long)x * N + ch * NB;
-        for (int rf = r0; rf < r1; rf += 4) {
-          float4 o = *reinterpret_cast<float4*>(orow + rf);
-          o.x += scale * (sm[oK + rf * PK + i] + sm[oK + (NB + rf) * PK + XB - 1 - i]);
-          o.y += scale * (sm[oK + (rf + 1) * PK + i] + sm[oK + (NB + rf + 1) * PK + XB - 1 - i]);
-          o.z += scale * (sm[oK + (rf + 2) * PK + i] + sm[oK + (NB + rf + 2) * PK + XB - 1 - i]);
-          o.w += scale * (sm[oK + (rf + 3) * PK + i] + sm[oK + (NB + rf + 3) * PK + XB - 1 - i]);
-          *reinterpret_cast<float4*>(orow + rf) = o;
-        }
+        const int rf = 4 * rq;
+        float4 o = ld4(oG + i * PG + rf);
+        o.x += scale * (sm[oIn + rf * PK + i] + sm[oIn + (NB + rf) * PK + XB - 1 - i]);
+        o.y += scale * (sm[oIn + (rf + 1) * PK + i] + sm[oIn + (NB + rf + 1) * PK + XB - 1 - i]);
+        o.z += scale * (sm[oIn + (rf + 2) * PK + i] + sm[oIn + (NB + rf + 2) * PK + XB - 1 - i]);
+        o.w += scale * (sm[oIn + (rf + 3) * PK + i] + sm[oIn + (NB + rf + 3) * PK + XB - 1 - i]);
+        *reinterpret_cast<float4*>(out + (long long)x * N + ch * NB + rf) = o;
       }
     }
-    if (tn >= nitems) break;
-    t = tn;
-    buf ^= 1;
+    __syncthreads();                                   // park / staging reused by the next item
   }
 }
 
@@ -743,8 +765,8 @@ size_t pair_b_smem(const SweepGeom& g) {
   const int O1 = (R1 == 3) ? 8 : 4;
   const int HS = pb_halo(R1, R2);
   const int HI = HS + O1;
-  const int PI = pitch4(HI + XB), PS = pitch4(HS + XB + 4), PK = XB + 4;
-  return ((size_t)4 * NB * PI + (size_t)2 * NB * PS + (size_t)2 * NB * PK) * sizeof(float);
+  const int PI = pitch4(HI + XB), PS = pitch4(HS + XB + 4), PG = NB + 4;
+  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG) * sizeof(float);
 }
 
 template <int H, int X, bool IIR, bool BETA>
@@ -788,10 +810,10 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
   return cudaErrorInvalidValue;
 }
 
-template <int R1, int R2, int XB>
-static cudaError_t launch_b_t(const float* R, float* img, int slices, int pair, float scale,
+template <int R1, int R2, int XB, int PAIR>
+static cudaError_t launch_b_t(const float* R, float* img, int slices, float scale,
                               const SweepGeom& g, cudaStream_t st) {
-  auto kern = k_pair_b<R1, R2, XB>;
+  auto kern = k_pair_b<R1, R2, XB, PAIR>;
   const size_t smem = pair_b_smem(g);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -802,7 +824,7 @@ static cudaError_t launch_b_t(const float* R, float* img, int slices, int pair, 
   if (per < 1) per = 1;
   const long long nitems = (long long)((g.N + g.XB - 1) / g.XB) * g.H * slices;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
-  kern<<<(unsigned)grid, 256, smem, st>>>(R, img, g, slices, pair, scale, nitems);
+  kern<<<(unsigned)grid, 256, smem, st>>>(R, img, g, scale, nitems);
   return cudaGetLastError();
 }
 
@@ -810,9 +832,14 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
                           const SweepGeom& g, cudaStream_t st, int* launches) {
   if (slices <= 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
-  if (g.XB != 128) return cudaErrorInvalidValue;
-  if (g.NB == 16) e = launch_b_t<2, 2, 128>(R, img, slices, pair, scale, g, st);
-  else if (g.NB == 32) e = launch_b_t<3, 2, 128>(R, img, slices, pair, scale, g, st);
+  if (g.XB != 128) return e;
+#define FBP_PAIR_CASE(NBV, R1, R2)                                                          \
+  if (g.NB == NBV)                                                                          \
+    e = pair == 0 ? launch_b_t<R1, R2, 128, 0>(R, img, slices, scale, g, st)                \
+                  : launch_b_t<R1, R2, 128, 1>(R, img, slices, scale, g, st);
+  FBP_PAIR_CASE(16, 2, 2)
+  FBP_PAIR_CASE(32, 3, 2)
+#undef FBP_PAIR_CASE
   if (launches) ++*launches;
   return e;
 }
