@@ -103,8 +103,8 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- roofline
-def kernel_algorithmic_bytes(kind: str, N: int, NB: int, H: int) -> float:
-    """Algorithmic HBM bytes per SLICE of each kernel (DESIGN.md §8)."""
+def kernel_algorithmic_bytes(kind: str, N: int, NB: int, H: int, path: dict | None = None) -> float:
+    """Algorithmic HBM bytes per SLICE of each kernel (DESIGN.md §7)."""
     W = 2 * N
     lin = 4.0 * N * W * 4                                  # 32 N^2 B
     # compact pass-A output: per family sum_b H rows of (N + b) floats
@@ -113,6 +113,12 @@ def kernel_algorithmic_bytes(kind: str, N: int, NB: int, H: int) -> float:
     if kind == "iir":
         return 2 * lin                                     # read S, write F
     if kind == "fht_pass_a":
+        if path and path.get("fast"):
+            # fused sweep: reads rows of block b from tile max(0, j0(b) - D), writes R
+            X, D = path["tile_width"], path["lookahead_tiles"]
+            nt = W // X
+            cols = sum((nt - max(0, (N - (b + 1) * H + 1) // X - D)) * X for b in range(NB))
+            return 4.0 * H * cols * 4 + 4 * r_fam
         return lin + 4 * r_fam                             # read F, write R
     if kind == "fht_pass_b":
         return 4 * r_fam + img + 2 * img                   # read R; write v-pair, RMW h-pair
@@ -282,7 +288,7 @@ def run_fbp(args):
         dom = max(kinds, key=lambda k: kinds[k][0])
         dom_ms, dom_n = kinds[dom]
         slices_per_launch = (B * args.steps) / dom_n if dom != "fht_pass_b" else (B * args.steps) / (dom_n / 2)
-        alg = kernel_algorithmic_bytes(dom, N, 1 << info["m"], 1 << info["k1"])
+        alg = kernel_algorithmic_bytes(dom, N, 1 << info["m"], 1 << info["k1"], plan.path())
         if dom == "fht_pass_b":
             alg = alg / 2                     # one launch = one family pair
         per_launch_bytes = alg * slices_per_launch

@@ -84,9 +84,11 @@ struct It {
 // start (virtual column col0 - O) of input row b' = 0; row b' lives at
 // w0 + b'*rowstep, pre-shift c*b' (the physical shift (c*b') & 3 was applied by
 // the producer, so the physical window starts 4*floor(c*b'/4) columns left).
+// Rows are held as column pairs (float2) so that the levels can add two columns
+// per FADD2 where the shift is even.
 template <int R, int C>
 __device__ __forceinline__ void item_load(int w0, int rowstep, int c,
-                                          float (&v)[It<R, C>::NR][It<R, C>::T]) {
+                                          float2 (&v)[It<R, C>::NR][It<R, C>::T / 2]) {
   constexpr int NR = It<R, C>::NR, T = It<R, C>::T;
   int cb = 0;
 #pragma unroll
@@ -96,26 +98,30 @@ __device__ __forceinline__ void item_load(int w0, int rowstep, int c,
 #pragma unroll
     for (int q = 0; q < T / 4; ++q) {
       const float4 f = ld4(off + 4 * q);
-      v[b][4 * q] = f.x;
-      v[b][4 * q + 1] = f.y;
-      v[b][4 * q + 2] = f.z;
-      v[b][4 * q + 3] = f.w;
+      v[b][2 * q] = make_float2(f.x, f.y);
+      v[b][2 * q + 1] = make_float2(f.z, f.w);
     }
   }
+}
+
+template <int T2>
+__device__ __forceinline__ float col(const float2 (&row)[T2], int t) {
+  return (t & 1) ? row[t >> 1].y : row[t >> 1].x;
 }
 
 // R levels in registers (natural recursion, compile-time shifts), computing at each
 // level only the window columns the outputs [O, T) depend on.
 //   level h -> 2h:  w[blk + y'][t] = v[blk + lo][t] + v[blk + h + lo][t - ceil(y'/2)],
 //   lo = floor(y'/2)  (negative shift direction)
+// Even shifts: one FADD2 per column pair; odd shifts: two FADDs.
 template <int R, int C>
-__device__ __forceinline__ void item_fht(float (&v)[It<R, C>::NR][It<R, C>::T]) {
-  constexpr int NR = It<R, C>::NR, T = It<R, C>::T, O = It<R, C>::O;
+__device__ __forceinline__ void item_fht(float2 (&v)[It<R, C>::NR][It<R, C>::T / 2]) {
+  constexpr int NR = It<R, C>::NR, T = It<R, C>::T, O = It<R, C>::O, T2 = T / 2;
 #pragma unroll
   for (int lvl = 0; lvl < R; ++lvl) {
     const int h = 1 << lvl;
-    const int lb = O - ((1 << R) - (1 << (lvl + 1)));
-    float w[NR][T];
+    const int lb = O - ((1 << R) - (1 << (lvl + 1)));   // even
+    float2 w[NR][T2];
 #pragma unroll
     for (int y = 0; y < NR; ++y) {
       const int blk = y & ~(2 * h - 1);
@@ -123,15 +129,21 @@ __device__ __forceinline__ void item_fht(float (&v)[It<R, C>::NR][It<R, C>::T]) 
       const int lo = yp >> 1;
       const int sh = (yp + 1) >> 1;
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        if (t >= lb) w[y][t] = (t >= sh) ? v[blk + lo][t] + v[blk + h + lo][t - sh] : v[blk + lo][t];
+      for (int tp = lb / 2; tp < T2; ++tp) {
+        const int t = 2 * tp;
+        const float2 a = v[blk + lo][tp];
+        if ((sh & 1) == 0) {
+          w[y][tp] = (t >= sh) ? __fadd2_rn(a, v[blk + h + lo][tp - sh / 2]) : a;
+        } else {
+          w[y][tp].x = (t >= sh) ? a.x + col(v[blk + h + lo], t - sh) : a.x;
+          w[y][tp].y = (t + 1 >= sh) ? a.y + col(v[blk + h + lo], t + 1 - sh) : a.y;
+        }
       }
     }
 #pragma unroll
     for (int y = 0; y < NR; ++y)
 #pragma unroll
-      for (int t = 0; t < T; ++t)
-        if (t >= lb) v[y][t] = w[y][t];
+      for (int tp = lb / 2; tp < T2; ++tp) v[y][tp] = w[y][tp];
   }
 }
 
@@ -258,12 +270,14 @@ __global__ void __launch_bounds__(H * X / 32)
   constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);   // step-2 input halo
   constexpr int PF = pitch4(HF + X + 4);
   constexpr int PS = pitch4(HS + X + 4);
-  constexpr int oF0 = 0, oF1 = H * PF, oS = 2 * H * PF, oRing = oS + H * PS;
+  constexpr int PL = pitch4(X + 4);                     // look-ahead slot pitch
+  // single F tile + an 8-column halo stash (the next tile's landing overwrites F)
+  constexpr int oF = 0, oStash = H * PF, oS = oStash + H * HF, oLA = oS + H * PS, oRing = oLA + H * PL;
   static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
 
   const int tid = threadIdx.x;
   const int D = g.D;
-  int* s_item = reinterpret_cast<int*>(sm + oRing + (D + 1) * H * 4);
+  int* s_item = reinterpret_cast<int*>(sm + oRing + (D + 1) * H * 3);
   const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
   const long long nsf = (long long)slices * nf;
   const long long nitems = nsf * NB;
@@ -309,60 +323,56 @@ __global__ void __launch_bounds__(H * X / 32)
       cp_commit();
     };
 
-    // look-ahead: anticausal aggregate of tile jt from registers -> ring
-    auto la_finish = [&](int jt, int slot, const float (&lx)[32], float ln0, float ln1) {
+    // look-ahead landing: tile jt (X + 4 columns: the next tile's first quad feeds
+    // the feedforward at the tile's right edge) into buffer `ob` (pitch `pl`),
+    // coalesced cp.async; columns beyond the row read as zero.
+    auto la_land = [&](int ob, int pl, int jt) {
+      constexpr int NQ = X / 4 + 1;
+      for (int e = tid; e < H * NQ; e += NT) {
+        const int r = e / NQ, qd = e - r * NQ;
+        const int gc = jt * X + 4 * qd;
+        const bool ok = (jt < nt) && (gc < W);
+        cp16(ob + r * pl + 4 * qd, ok ? src + (long long)r * W + gc : src, ok);
+      }
+      cp_commit();
+    };
+    // look-ahead: anticausal aggregate of landed tile jt -> ring slot
+    auto la_finish = [&](int ob, int pl, int jt, int slot) {
+      const int rowL = ob + ir * pl + 32 * iq;
+      float lx[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = ld4(rowL + 4 * q);
+        lx[4 * q] = v.x;
+        lx[4 * q + 1] = v.y;
+        lx[4 * q + 2] = v.z;
+        lx[4 * q + 3] = v.w;
+      }
+      const float4 nx = ld4(rowL + 32);        // next chunk (or next tile) first samples
       float va[3];
-      // right neighbours of this chunk: next chunk's first two samples (or next tile's)
-      const float p0 = __shfl_down_sync(0xffffffffu, lx[0], 8);
-      const float p1 = __shfl_down_sync(0xffffffffu, lx[1], 8);
-      const float xn0 = (iq == TPR - 1) ? ln0 : p0;
-      const float xn1 = (iq == TPR - 1) ? ln1 : p1;
-      chunk_anticausal_state<BETA>(lx, xn0, xn1, k, va);
+      chunk_anticausal_state<BETA>(lx, nx.x, nx.y, k, va);
       // suffix combine over the row's chunks: agg = sum_q (A^32)^q va_q
-      P3 S;
-      S.s0 = make_float2(va[0], 0.f);
-      S.s1 = make_float2(va[1], 0.f);
-      S.s2 = make_float2(va[2], 0.f);
+      float S0 = va[0], S1v = va[1], S2 = va[2];
 #pragma unroll
       for (int st = 0; (1 << st) < TPR; ++st) {
         const int off = 8 << st;
-        P3 o;
-        o.s0 = make_float2(__shfl_down_sync(0xffffffffu, S.s0.x, off), 0.f);
-        o.s1 = make_float2(__shfl_down_sync(0xffffffffu, S.s1.x, off), 0.f);
-        o.s2 = make_float2(__shfl_down_sync(0xffffffffu, S.s2.x, off), 0.f);
-        const P3 t = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
+        const float o[3] = {__shfl_down_sync(0xffffffffu, S0, off), __shfl_down_sync(0xffffffffu, S1v, off),
+                            __shfl_down_sync(0xffffffffu, S2, off)};
+        float t[3] = {0.f, 0.f, 0.f};
+        if (st == 0) mv1(k.M1, o, t);
+        else mv1(k.M2, o, t);
         if (iq + (1 << st) < TPR) {
-          S.s0.x += t.s0.x;
-          S.s1.x += t.s1.x;
-          S.s2.x += t.s2.x;
+          S0 += t[0];
+          S1v += t[1];
+          S2 += t[2];
         }
       }
       if (iq == 0) {
         const bool live = jt < nt;
-        st4(oRing + (slot * H + ir) * 4,
-            make_float4(live ? S.s0.x : 0.f, live ? S.s1.x : 0.f, live ? S.s2.x : 0.f, 0.f));
-      }
-    };
-    auto la_load = [&](int jt, float (&lx)[32], float& ln0, float& ln1) {
-      ln0 = ln1 = 0.f;
-      if (jt < nt) {
-        const float* p = src + (long long)ir * W + jt * X + 32 * iq;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
-          lx[4 * q] = v.x;
-          lx[4 * q + 1] = v.y;
-          lx[4 * q + 2] = v.z;
-          lx[4 * q + 3] = v.w;
-        }
-        if (iq == TPR - 1 && jt + 1 < nt) {
-          const float2 v = __ldg(reinterpret_cast<const float2*>(p + 32));
-          ln0 = v.x;
-          ln1 = v.y;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) lx[q] = 0.f;
+        const int o = oRing + (slot * H + ir) * 3;
+        sm[o] = live ? S0 : 0.f;
+        sm[o + 1] = live ? S1v : 0.f;
+        sm[o + 2] = live ? S2 : 0.f;
       }
     };
 
@@ -376,33 +386,37 @@ __global__ void __launch_bounds__(H * X / 32)
         prefetch_line(src + (long long)r * W + jst * X + 32 * rest);
       }
     }
-    land(oF0, jst);
+    land(oF, jst);
     float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
     if (IIR) {
-      for (int i = 1; i <= D; ++i) {
-        float lx[32], ln0, ln1;
-        la_load(jst + i, lx, ln0, ln1);
-        la_finish(jst + i, i, lx, ln0, ln1);       // tile jst + i -> slot i
+      // prologue look-ahead: tiles jst+1 .. jst+D in batches of two buffers
+      // (LA slot and S1 are free before the first step)
+      for (int i0 = 1; i0 <= D; i0 += 2) {
+        const int nb = min(2, D - i0 + 1);
+        for (int k2 = 0; k2 < nb; ++k2)
+          la_land(k2 == 0 ? oLA : oS, k2 == 0 ? PL : PS, jst + i0 + k2);
+        cp_wait<0>();
+        __syncthreads();
+        for (int k2 = 0; k2 < nb; ++k2)
+          la_finish(k2 == 0 ? oLA : oS, k2 == 0 ? PL : PS, jst + i0 + k2, i0 + k2);   // tile jst+i -> slot i
+        __syncthreads();
       }
     }
     int slot_j = 0;                                    // ring slot of tile j (j - jst mod D+1)
 
     for (int j = jst; j < nt; ++j) {
-      const int cur = (j - jst) & 1;
-      const int oFc = cur ? oF1 : oF0;
-      const int oFp = cur ? oF0 : oF1;
+      const int oFc = oF;
       {
         const int jp = j + (IIR ? D + 1 : 0) + g.P + 1;
         constexpr int LPR = X / 32;
         if (jp < nt && tid < H * LPR)
           prefetch_line(src + (long long)(tid % H) * W + jp * X + 32 * (tid / H));
       }
-      float lx[32], ln0 = 0.f, ln1 = 0.f;
       const int jl = j + D + 1;
-      if (IIR) la_load(jl, lx, ln0, ln1);
 
       cp_wait<0>();
       __syncthreads();
+      if (IIR) la_land(oLA, PL, jl);                    // consumed at the end of this step
 
       if (IIR) {
         // ---- local sweeps of this thread's chunk ----
@@ -425,14 +439,13 @@ __global__ void __launch_bounds__(H * X / 32)
         {
           int sl = slot_j + D;                             // slot of tile j + D
           if (sl > D) sl -= D + 1;
-          const float4 a = ld4(oRing + (sl * H + ir) * 4);
-          tm[0] = a.x;
-          tm[1] = a.y;
-          tm[2] = a.z;
+          tm[0] = sm[oRing + (sl * H + ir) * 3];
+          tm[1] = sm[oRing + (sl * H + ir) * 3 + 1];
+          tm[2] = sm[oRing + (sl * H + ir) * 3 + 2];
           for (int i = D - 1; i >= 1; --i) {
             sl = (sl == 0) ? D : sl - 1;                     // slot of tile j + i
-            const float4 c = ld4(oRing + (sl * H + ir) * 4);
-            float acc[3] = {c.x, c.y, c.z};
+            float acc[3] = {sm[oRing + (sl * H + ir) * 3], sm[oRing + (sl * H + ir) * 3 + 1],
+                            sm[oRing + (sl * H + ir) * 3 + 2]};
             mv1(k.MX, tm, acc);
             tm[0] = acc[0];
             tm[1] = acc[1];
@@ -519,7 +532,7 @@ __global__ void __launch_bounds__(H * X / 32)
         // halo: previous tile's last HF filtered columns (zero before the first tile)
         for (int e = tid; e < 2 * H; e += NT) {
           const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + r * PF + X + 4 * qd);
+          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
           st4(oFc + r * PF + 4 * qd, h);
         }
 #pragma unroll
@@ -531,18 +544,17 @@ __global__ void __launch_bounds__(H * X / 32)
       } else {
         for (int e = tid; e < 2 * H; e += NT) {
           const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + r * PF + X + 4 * qd);
+          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
           st4(oFc + r * PF + 4 * qd, h);
         }
       }
       __syncthreads();                                   // F tile complete
-      if (j + 1 < nt) land(oFp, j + 1);
 
       // ---- FHT step 1 (levels 1-3): F -> S1 ----
       if (j >= j0) {
         constexpr int NCH = X / C1;
         const int jj = tid % NCH, G = tid / NCH;
-        float v[8][It<3, C1>::T];
+        float2 v[8][It<3, C1>::T / 2];
         item_load<3, C1>(oFc + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
         item_fht<3, C1>(v);
         const int gb = G & (NR2 - 1);                   // next step's block index
@@ -550,15 +562,21 @@ __global__ void __launch_bounds__(H * X / 32)
         for (int r = 0; r < 8; ++r) {
           const int o = oS + (G * 8 + r) * PS + HS + C1 * jj + ((r * gb) & 3);
 #pragma unroll
-          for (int t = 0; t < C1; ++t) sm[o + t] = v[r][It<3, C1>::O + t];
+          for (int t = 0; t < C1; ++t) sm[o + t] = col(v[r], It<3, C1>::O + t);
         }
       }
+      // stash this tile's last HF filtered columns (halo of the next tile)
+      for (int e = tid; e < 2 * H; e += NT) {
+        const int r = e >> 1, qd = e & 1;
+        st4(oStash + r * HF + 4 * qd, ld4(oFc + r * PF + X + 4 * qd));
+      }
       __syncthreads();
+      if (j + 1 < nt) land(oF, j + 1);                   // F is free: step 1 has read it
       // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
       if (j >= j0) {
         constexpr int NCH = X / C2;
         const int jj = tid % NCH, c = tid / NCH;
-        float v[NR2][It<R2, C2>::T];
+        float2 v[NR2][It<R2, C2>::T / 2];
         item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
         item_fht<R2, C2>(v);
         const int ubase = j * X + C2 * jj;
@@ -570,25 +588,35 @@ __global__ void __launch_bounds__(H * X / 32)
           float* o = dstR + (long long)cf * WR + (cf * b - N + NB);
           if (ubase >= ulo && ubase + C2 <= uhi) {
 #pragma unroll
-            for (int t = 0; t < C2; ++t) o[ubase + t] = v[r][O2 + t];
+            for (int t = 0; t < C2; ++t) o[ubase + t] = col(v[r], O2 + t);
           } else if (ubase + C2 > ulo && ubase < uhi) {
 #pragma unroll
             for (int t = 0; t < C2; ++t) {
               const int u = ubase + t;
-              if (u >= ulo && u < uhi) o[u] = v[r][O2 + t];
+              if (u >= ulo && u < uhi) o[u] = col(v[r], O2 + t);
             }
           }
         }
       }
-      if (IIR) la_finish(jl, slot_j, lx, ln0, ln1);   // tile j + D + 1 reuses tile j's slot
-      slot_j = (slot_j == D) ? 0 : slot_j + 1;
+      if (IIR) {
+        // look-ahead group issued this step; the landing of j + 1 (if any) is newer
+        if (j + 1 < nt) cp_wait<1>(); else cp_wait<0>();
+      }
       __syncthreads();
-      // ---- S1 halo for the next tile ----
+      if (IIR) la_finish(oLA, PL, jl, slot_j);          // tile j + D + 1 reuses tile j's slot
+      slot_j = (slot_j == D) ? 0 : slot_j + 1;
+      // ---- S1 halo for the next tile: row (b', c) of step 2 reads virtual columns
+      //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
       if (j >= j0) {
-        constexpr int NQ = (HS + 4) / 4;
-        for (int e = tid; e < H * NQ; e += NT) {
-          const int r = e / NQ, qd = e - r * NQ;
-          st4(oS + r * PS + 4 * qd, ld4(oS + r * PS + X + 4 * qd));
+        constexpr int MAXQ = (HS + 4) / 4;
+        const int r = tid >> 1;
+        for (int rr = r; rr < H; rr += NT / 2) {
+          const int cb = (rr & 7) * (rr >> 3);
+          const int nq = (O2 + (cb & ~3)) / 4 + 1;
+          for (int qd = tid & 1; qd < nq && qd < MAXQ; qd += 2) {
+            const int c0 = HS + 4 - 4 * (qd + 1);
+            st4(oS + rr * PS + c0, ld4(oS + rr * PS + X + c0));
+          }
         }
       }
     }
@@ -673,14 +701,14 @@ __global__ void __launch_bounds__(256, 2)
         const int q = it / per_fam;
         const int r3 = it - q * per_fam;
         const int G = r3 / nch, jj = r3 - G * nch;
-        float v[NR1][It<R1, C1>::T];
+        float2 v[NR1][It<R1, C1>::T / 2];
         item_load<R1, C1>(oIn + (q * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
         item_fht<R1, C1>(v);
 #pragma unroll
         for (int r = 0; r < NR1; ++r) {
           const int o = oS + (q * NB + G * NR1 + r) * PS + C1 * jj + ((r * G) & 3);
 #pragma unroll
-          for (int tt = 0; tt < C1; ++tt) sm[o + tt] = v[r][O1 + tt];
+          for (int tt = 0; tt < C1; ++tt) sm[o + tt] = col(v[r], O1 + tt);
         }
       }
     }
@@ -693,7 +721,7 @@ __global__ void __launch_bounds__(256, 2)
         const int q = it / per_fam;
         const int r3 = it - q * per_fam;
         const int c = r3 / nch, jj = r3 - c * nch;
-        float v[NR2][It<R2, C2>::T];
+        float2 v[NR2][It<R2, C2>::T / 2];
         item_load<R2, C2>(oS + (q * NB + c) * PS + HS + C2 * jj - O2, NR1 * PS, c, v);
         item_fht<R2, C2>(v);
 #pragma unroll
@@ -702,10 +730,11 @@ __global__ void __launch_bounds__(256, 2)
           if (PAIR == 0) {
 #pragma unroll
             for (int tt = 0; tt < C2; tt += 4)
-              st4(o + tt, make_float4(v[r][O2 + tt], v[r][O2 + tt + 1], v[r][O2 + tt + 2], v[r][O2 + tt + 3]));
+              st4(o + tt, make_float4(col(v[r], O2 + tt), col(v[r], O2 + tt + 1), col(v[r], O2 + tt + 2),
+                                      col(v[r], O2 + tt + 3)));
           } else {
 #pragma unroll
-            for (int tt = 0; tt < C2; ++tt) sm[o + tt] = v[r][O2 + tt];
+            for (int tt = 0; tt < C2; ++tt) sm[o + tt] = col(v[r], O2 + tt);
           }
         }
       }
@@ -753,8 +782,9 @@ size_t sweep_a_smem(const SweepGeom& g) {
   const int R2 = (H == 64) ? 3 : 2;
   const int O2 = 4;
   const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : O2 + 4 * ((7 * 3) / 4);
-  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
-  return ((size_t)2 * H * PF + (size_t)H * PS + (size_t)(g.D + 1) * H * 4 + 4) * sizeof(float);
+  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4), PL = pitch4(X + 4);
+  return ((size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4) *
+         sizeof(float);
 }
 
 size_t pair_b_smem(const SweepGeom& g) {
