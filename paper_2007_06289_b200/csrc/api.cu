@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -352,8 +353,9 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.WR = p->g.WR;
     sg.X = 4096 / sg.H;
     sg.nt = sg.W / sg.X;
-    sg.P = 4;
+    sg.P = 0;   // look-ahead reads are a full step (~6 us) ahead of use: no extra prefetch
     sg.XB = 128;
+    if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
     // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
     const int K = 1 << 16;
     std::vector<double> h(K, 0.0);

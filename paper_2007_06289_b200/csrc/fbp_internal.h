@@ -66,6 +66,7 @@ struct SweepGeom {
   int D;      // look-ahead tiles for the anticausal carry (plan: tail bound)
   int P;      // L2 prefetch distance in tiles
   int XB;     // pass-B x-tile width
+  int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
 };
 
 // Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at

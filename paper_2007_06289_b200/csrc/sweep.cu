@@ -49,6 +49,22 @@ __device__ __forceinline__ void cp16(int soff, const float* g, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sm + soff);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 16 : 0));
 }
+// cp.async with an L2 cache policy (createpolicy): second reads of linogram tiles
+// are marked evict-first so that they do not displace tiles still ahead.
+__device__ __forceinline__ void cp16h(int soff, const float* g, bool valid, unsigned long long pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sm + soff);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(g),
+               "r"(valid ? 16 : 0), "l"(pol));
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+// streaming store of the compact R rows (read back only by the next launch)
+__device__ __forceinline__ void st_ef(float* g, float v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(g), "f"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int NLEFT>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
@@ -256,7 +272,7 @@ __device__ __forceinline__ float2 shfl_up2(float2 v, int d) {
 //   ring   : (D+1) x H x 4  anticausal tile aggregates
 // ===========================================================================
 template <int H, int X, bool IIR, bool BETA>
-__global__ void __launch_bounds__(H * X / 32)
+__global__ void __launch_bounds__(H * X / 32, 3)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
               int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter) {
   constexpr int NT = H * X / 32;
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(H * X / 32)
   const int iq = (tid >> 3) % TPR;
   const int ir = (tid & 7) + 8 * (tid / (8 * TPR));
   const int lane = tid & 31;
+  const unsigned long long pol_ef = policy_evict_first();
 
   while (true) {
     __syncthreads();
@@ -309,30 +326,44 @@ __global__ void __launch_bounds__(H * X / 32)
     const int j0 = (N - (b + 1) * H + 1) / X;
     const int jst = IIR ? max(0, j0 - D) : j0;
 
-    // landing of tile jt into F buffer `ofb` (IIR: with one quad of neighbours each side)
-    auto land = [&](int ofb, int jt) {
-      constexpr int NQ = IIR ? (X + 8) / 4 : X / 4;
-      constexpr int c0 = IIR ? HF - 4 : HF;
-      const int g0 = jt * X - (IIR ? 4 : 0);
-      for (int e = tid; e < H * NQ; e += NT) {
-        const int r = e / NQ, qd = e - r * NQ;
-        const int gc = g0 + 4 * qd;
+    // Copy roles: lanes cover whole 128-byte lines -- LQ = min(32, X/4) consecutive
+    // quads of a row per lane group, 32/LQ rows per warp instruction, RR rows per
+    // round of the CTA, H/RR rounds (row stride RR: immediate address offsets).
+    constexpr int LQ = (X / 4 < 32) ? X / 4 : 32;
+    constexpr int RR = (NT / 32) * (32 / LQ);
+    constexpr int ROUNDS = H / RR;
+    static_assert(X / 4 == LQ && H % RR == 0, "landing tiling");
+    const int cr = (tid / 32) * (32 / LQ) + (tid % 32) / LQ, cq = tid % LQ;
+    const float* crow = src + (long long)cr * W + 4 * cq;
+    // landing of tile jt into the F tile (IIR: with one quad of neighbours each side)
+    auto land = [&](int jt) {
+      const float* g = crow + jt * X;
+      const int so = oF + cr * PF + HF + 4 * cq;
+#pragma unroll
+      for (int k = 0; k < ROUNDS; ++k) cp16h(so + RR * PF * k, g + (long long)RR * W * k, true, pol_ef);
+      if (IIR && tid < 2 * H) {
+        const int r = tid >> 1, side = tid & 1;           // side 0: left quad, 1: right quad
+        const int gc = side ? (jt + 1) * X : jt * X - 4;
         const bool ok = (gc >= 0) && (gc < W);
-        cp16(ofb + r * PF + c0 + 4 * qd, ok ? src + (long long)r * W + gc : src, ok);
+        cp16h(oF + r * PF + (side ? HF + X : HF - 4), ok ? src + (long long)r * W + gc : src, ok, pol_ef);
       }
       cp_commit();
     };
 
     // look-ahead landing: tile jt (X + 4 columns: the next tile's first quad feeds
-    // the feedforward at the tile's right edge) into buffer `ob` (pitch `pl`),
-    // coalesced cp.async; columns beyond the row read as zero.
+    // the feedforward at the tile's right edge) into buffer `ob` (pitch `pl`);
+    // nothing is loaded for tiles beyond the row, columns beyond it read as zero.
     auto la_land = [&](int ob, int pl, int jt) {
-      constexpr int NQ = X / 4 + 1;
-      for (int e = tid; e < H * NQ; e += NT) {
-        const int r = e / NQ, qd = e - r * NQ;
-        const int gc = jt * X + 4 * qd;
-        const bool ok = (jt < nt) && (gc < W);
-        cp16(ob + r * pl + 4 * qd, ok ? src + (long long)r * W + gc : src, ok);
+      if (jt < nt) {
+        const float* g = crow + jt * X;
+        const int so = ob + cr * pl + 4 * cq;
+#pragma unroll
+        for (int k = 0; k < ROUNDS; ++k) cp16(so + RR * pl * k, g + (long long)RR * W * k, true);
+        if (tid < H) {
+          const int gc = (jt + 1) * X;
+          const bool ok = gc < W;
+          cp16(ob + tid * pl + X, ok ? src + (long long)tid * W + gc : src, ok);
+        }
       }
       cp_commit();
     };
@@ -386,7 +417,7 @@ __global__ void __launch_bounds__(H * X / 32)
         prefetch_line(src + (long long)r * W + jst * X + 32 * rest);
       }
     }
-    land(oF, jst);
+    land(jst);
     float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
     if (IIR) {
       // prologue look-ahead: tiles jst+1 .. jst+D in batches of two buffers
@@ -409,7 +440,7 @@ __global__ void __launch_bounds__(H * X / 32)
       {
         const int jp = j + (IIR ? D + 1 : 0) + g.P + 1;
         constexpr int LPR = X / 32;
-        if (jp < nt && tid < H * LPR)
+        if (g.P > 0 && jp < nt && tid < H * LPR)
           prefetch_line(src + (long long)(tid % H) * W + jp * X + 32 * (tid / H));
       }
       const int jl = j + D + 1;
@@ -571,7 +602,7 @@ __global__ void __launch_bounds__(H * X / 32)
         st4(oStash + r * HF + 4 * qd, ld4(oFc + r * PF + X + 4 * qd));
       }
       __syncthreads();
-      if (j + 1 < nt) land(oF, j + 1);                   // F is free: step 1 has read it
+      if (j + 1 < nt) land(j + 1);                       // F is free: step 1 has read it
       // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
       if (j >= j0) {
         constexpr int NCH = X / C2;
@@ -588,12 +619,12 @@ __global__ void __launch_bounds__(H * X / 32)
           float* o = dstR + (long long)cf * WR + (cf * b - N + NB);
           if (ubase >= ulo && ubase + C2 <= uhi) {
 #pragma unroll
-            for (int t = 0; t < C2; ++t) o[ubase + t] = col(v[r], O2 + t);
+            for (int t = 0; t < C2; ++t) st_ef(o + ubase + t, col(v[r], O2 + t), pol_ef);
           } else if (ubase + C2 > ulo && ubase < uhi) {
 #pragma unroll
             for (int t = 0; t < C2; ++t) {
               const int u = ubase + t;
-              if (u >= ulo && u < uhi) o[u] = col(v[r], O2 + t);
+              if (u >= ulo && u < uhi) st_ef(o + u, col(v[r], O2 + t), pol_ef);
             }
           }
         }
@@ -647,7 +678,9 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int O1 = It<R1, C1>::O, O2 = It<R2, C2>::O;
   constexpr int HS = pb_halo(R1, R2);
   constexpr int HI = HS + O1;
-  constexpr int PI = pitch4(HI + XB);
+  constexpr int RPT = NT / (2 * NB);                  // fill threads per input row
+  constexpr int NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;   // filled quads per row
+  constexpr int PI = pitch4(4 * NQF);
   constexpr int PS = pitch4(HS + XB + 4);
   constexpr int PK = PAIR == 0 ? XB + 4 : XB + 1;     // pair 1 reads park columns
   constexpr int PG = NB + 4;                          // image staging pitch (pair 1)
@@ -667,26 +700,52 @@ __global__ void __launch_bounds__(256, 2)
     const int ch = rem / nx;
     const int x0 = (rem - ch * nx) * XB;
     float* out = img + sl * (long long)N * N;
-    // ---- fills: both families' compact rows (+ image rows for pair 1) ----
+    // ---- fills: both families' compact rows (+ image rows for pair 1); lanes cover
+    //      consecutive quads of a row (whole 128-byte lines) ----
     {
-      constexpr int nq = (HI + XB) / 4;
-      for (int e = tid; e < 2 * NB * nq; e += NT) {
-        const int q = e / (NB * nq);
-        const int r2 = e - q * NB * nq;
-        const int bq = r2 / nq, qd = r2 - bq * nq;
+      constexpr int nq = NQF;                            // quads per row (>= (HI+XB)/4)
+      constexpr int NROW = 2 * NB;
+      constexpr int W32 = nq / 32, TAIL = nq % 32;       // full 32-quad blocks, tail quads
+      const int lane = tid & 31, warp = tid >> 5;
+      auto row_src = [&](int rr, int& jp0, const float*& row) {
+        const int q = rr / NB, bq = rr % NB;
         const int xs = (q == 0) ? x0 : (N - x0 - XB);
-        const int jp = xs - HI + NB + 4 * qd;         // compact column j' = v - N + NB
-        const float* row = Rin + ((((sl * 4 + 2 * PAIR + q) * NB + bq) * (long long)H) + ch) * WR;
-        const bool ok = (jp >= 0) && (jp < WR);
-        cp16(oIn + (q * NB + bq) * PI + 4 * qd, ok ? row + jp : row, ok);
+        jp0 = xs - HI + NB;                              // compact column j' = v - N + NB
+        row = Rin + ((((sl * 4 + 2 * PAIR + q) * NB + bq) * (long long)H) + ch) * WR;
+      };
+      for (int rr = warp; rr < NROW; rr += NT / 32) {
+        int jp0;
+        const float* row;
+        row_src(rr, jp0, row);
+#pragma unroll
+        for (int kb = 0; kb < W32; ++kb) {
+          const int jp = jp0 + 4 * (32 * kb + lane);
+          const bool ok = (jp >= 0) && (jp < WR);
+          cp16(oIn + rr * PI + 4 * (32 * kb + lane), ok ? row + jp : row, ok);
+        }
+      }
+      if (TAIL > 0) {
+        constexpr int RPI = 32 / TAIL > 0 ? 32 / TAIL : 1;   // rows per warp instruction
+        for (int rb = warp * RPI; rb < NROW; rb += (NT / 32) * RPI) {
+          const int rr = rb + lane / TAIL;
+          if (lane / TAIL < RPI && rr < NROW) {
+            int jp0;
+            const float* row;
+            row_src(rr, jp0, row);
+            const int qd = 32 * W32 + lane % TAIL;
+            const int jp = jp0 + 4 * qd;
+            const bool ok = (jp >= 0) && (jp < WR);
+            cp16(oIn + rr * PI + 4 * qd, ok ? row + jp : row, ok);
+          }
+        }
       }
       if (PAIR == 1) {
-        constexpr int gq = NB / 4;
-        for (int e = tid; e < XB * gq; e += NT) {
-          const int i = e / gq, qd = e - i * gq;
+        constexpr int gq = NB / 4;                       // quads per staged image row
+        constexpr int RPI = 32 / gq;                     // image rows per warp instruction
+        for (int i0 = warp * RPI; i0 < XB; i0 += (NT / 32) * RPI) {
+          const int i = i0 + lane / gq, qd = lane % gq;
           const bool ok = x0 + i < N;
-          const float* src = out + (long long)(ok ? x0 + i : 0) * N + ch * NB + 4 * qd;
-          cp16(oG + i * PG + 4 * qd, src, ok);
+          cp16(oG + i * PG + 4 * qd, out + (long long)(ok ? x0 + i : 0) * N + ch * NB + 4 * qd, ok);
         }
       }
       cp_commit();
@@ -795,7 +854,8 @@ size_t pair_b_smem(const SweepGeom& g) {
   const int O1 = (R1 == 3) ? 8 : 4;
   const int HS = pb_halo(R1, R2);
   const int HI = HS + O1;
-  const int PI = pitch4(HI + XB), PS = pitch4(HS + XB + 4), PG = NB + 4;
+  const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
+  const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB + 4;
   return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG) * sizeof(float);
 }
 
@@ -811,6 +871,7 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, H * X / 32, smem);
+  if (g.ctas_a > 0 && g.ctas_a < per) per = g.ctas_a;   // tuning knob (FBP_SWEEP_CTAS)
   if (per < 1) per = 1;
   const long long nitems = (long long)slices * nf * g.NB;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
