@@ -67,6 +67,7 @@ struct SweepGeom {
   int P;      // L2 prefetch distance in tiles
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
+  int ws;     // use the warp-specialized sweep where available (env FBP_SWEEP_WS=0 disables)
 };
 
 // Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at
