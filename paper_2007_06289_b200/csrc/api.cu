@@ -356,7 +356,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.P = 0;   // look-ahead reads are a full step (~6 us) ahead of use: no extra prefetch
     sg.XB = 128;
     if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
-    sg.ws = 1;
+    sg.ws = 0;   // the warp-specialized variant (FBP_SWEEP_WS=1) measured slower than KS with TMA
     if (const char* ev = std::getenv("FBP_SWEEP_WS")) sg.ws = std::atoi(ev);
     // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
     const int K = 1 << 16;

@@ -71,6 +71,33 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int NLEFT>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier ----
+__device__ __forceinline__ unsigned smem_u32(int off) { return (unsigned)__cvta_generic_to_shared(sm + off); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// 2D tile box (cols c0.., rows r0..) of the linogram -> shared memory, completing on `bar`.
+// Out-of-range columns (c0 < 0 or beyond 2N) are zero-filled by the TMA unit.
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int r0, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(r0), "r"(bar)
+      : "memory");
+}
+
+
 __device__ __forceinline__ void prefetch_line(const float* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -276,7 +303,8 @@ __device__ __forceinline__ float2 shfl_up2(float2 v, int d) {
 template <int H, int X, bool IIR, bool BETA>
 __global__ void __launch_bounds__(H * X / 32, 3)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
-              int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter) {
+              int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter,
+              const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapL) {
   constexpr int NT = H * X / 32;
   constexpr int TPR = X / 32;                 // chunks (threads) per row in the IIR
   constexpr int R2 = (H == 64) ? 3 : 2;       // k1 = 3 + R2
@@ -295,7 +323,15 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 
   const int tid = threadIdx.x;
   const int D = g.D;
-  int* s_item = reinterpret_cast<int*>(sm + oRing + (D + 1) * H * 3);
+  // 3 mbarriers (F tile, look-ahead slot, prologue temp in S1), then the work item
+  const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
+  int* s_item = reinterpret_cast<int*>(sm + oBar + 6);
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph = 0;                                       // phase bits of the 3 mbarriers
   const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
   const long long nsf = (long long)slices * nf;
   const long long nitems = nsf * NB;
@@ -328,47 +364,29 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     const int j0 = (N - (b + 1) * H + 1) / X;
     const int jst = IIR ? max(0, j0 - D) : j0;
 
-    // Copy roles: lanes cover whole 128-byte lines -- LQ = min(32, X/4) consecutive
-    // quads of a row per lane group, 32/LQ rows per warp instruction, RR rows per
-    // round of the CTA, H/RR rounds (row stride RR: immediate address offsets).
-    constexpr int LQ = (X / 4 < 32) ? X / 4 : 32;
-    constexpr int RR = (NT / 32) * (32 / LQ);
-    constexpr int ROUNDS = H / RR;
-    static_assert(X / 4 == LQ && H % RR == 0, "landing tiling");
-    const int cr = (tid / 32) * (32 / LQ) + (tid % 32) / LQ, cq = tid % LQ;
-    const float* crow = src + (long long)cr * W + 4 * cq;
-    // landing of tile jt into the F tile (IIR: with one quad of neighbours each side)
-    auto land = [&](int jt) {
-      const float* g = crow + jt * X;
-      const int so = oF + cr * PF + HF + 4 * cq;
-#pragma unroll
-      for (int k = 0; k < ROUNDS; ++k) cp16h(so + RR * PF * k, g + (long long)RR * W * k, true, pol_ef);
-      if (IIR && tid < 2 * H) {
-        const int r = tid >> 1, side = tid & 1;           // side 0: left quad, 1: right quad
-        const int gc = side ? (jt + 1) * X : jt * X - 4;
-        const bool ok = (gc >= 0) && (gc < W);
-        cp16h(oF + r * PF + (side ? HF + X : HF - 4), ok ? src + (long long)r * W + gc : src, ok, pol_ef);
+    // TMA landings (thread 0 issues; every thread waits on the mbarrier):
+    //   F tile : box of H rows x PF columns from column jt*X - 8 (halo room, left
+    //            neighbour quad, core, right neighbour quad; zero-filled outside the row)
+    //   look-ahead: box of H rows x PL columns from column jt*X
+    const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
+    auto tma_issue = [&](const CUtensorMap* mp, int ob, int col, unsigned bytes, int bi) {
+      if (tid == 0) {
+        fence_proxy_async();
+        const unsigned bar = smem_u32(oBar + 2 * bi);
+        mbar_expect_tx(bar, bytes);
+        tma_load_2d(smem_u32(ob), mp, col, trow, bar);
       }
-      cp_commit();
+    };
+    auto tma_wait = [&](int bi) {
+      mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
+      ph ^= 1u << bi;
+    };
+    auto land = [&](int jt) { tma_issue(&tmapF, oF, jt * X - 8, H * PF * 4, 0); };
+    auto la_land = [&](int ob, int pl, int jt, int bi) {
+      (void)pl;
+      if (jt < nt) tma_issue(&tmapL, ob, jt * X, H * PL * 4, bi);
     };
 
-    // look-ahead landing: tile jt (X + 4 columns: the next tile's first quad feeds
-    // the feedforward at the tile's right edge) into buffer `ob` (pitch `pl`);
-    // nothing is loaded for tiles beyond the row, columns beyond it read as zero.
-    auto la_land = [&](int ob, int pl, int jt) {
-      if (jt < nt) {
-        const float* g = crow + jt * X;
-        const int so = ob + cr * pl + 4 * cq;
-#pragma unroll
-        for (int k = 0; k < ROUNDS; ++k) cp16(so + RR * pl * k, g + (long long)RR * W * k, true);
-        if (tid < H) {
-          const int gc = (jt + 1) * X;
-          const bool ok = gc < W;
-          cp16(ob + tid * pl + X, ok ? src + (long long)tid * W + gc : src, ok);
-        }
-      }
-      cp_commit();
-    };
     // look-ahead: anticausal aggregate of landed tile jt -> ring slot
     auto la_finish = [&](int ob, int pl, int jt, int slot) {
       const int rowL = ob + ir * pl + 32 * iq;
@@ -426,12 +444,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       // (LA slot and S1 are free before the first step)
       for (int i0 = 1; i0 <= D; i0 += 2) {
         const int nb = min(2, D - i0 + 1);
+        for (int k2 = 0; k2 < nb; ++k2) la_land(k2 == 0 ? oLA : oS, PL, jst + i0 + k2, k2 == 0 ? 1 : 2);
         for (int k2 = 0; k2 < nb; ++k2)
-          la_land(k2 == 0 ? oLA : oS, k2 == 0 ? PL : PS, jst + i0 + k2);
-        cp_wait<0>();
-        __syncthreads();
+          if (jst + i0 + k2 < nt) tma_wait(k2 == 0 ? 1 : 2);
         for (int k2 = 0; k2 < nb; ++k2)
-          la_finish(k2 == 0 ? oLA : oS, k2 == 0 ? PL : PS, jst + i0 + k2, i0 + k2);   // tile jst+i -> slot i
+          la_finish(k2 == 0 ? oLA : oS, PL, jst + i0 + k2, i0 + k2);   // tile jst+i -> slot i
         __syncthreads();
       }
     }
@@ -447,9 +464,9 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       }
       const int jl = j + D + 1;
 
-      cp_wait<0>();
-      __syncthreads();
-      if (IIR) la_land(oLA, PL, jl);                    // consumed at the end of this step
+      tma_wait(0);                                      // F tile of step j landed
+      __syncthreads();                                  // previous step's look-ahead reads done
+      if (IIR) la_land(oLA, PL, jl, 1);                 // consumed at the end of this step
 
       if (IIR) {
         // ---- local sweeps of this thread's chunk ----
@@ -631,10 +648,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           }
         }
       }
-      if (IIR) {
-        // look-ahead group issued this step; the landing of j + 1 (if any) is newer
-        if (j + 1 < nt) cp_wait<1>(); else cp_wait<0>();
-      }
+      if (IIR && jl < nt) tma_wait(1);
       __syncthreads();
       if (IIR) la_finish(oLA, PL, jl, slot_j);          // tile j + D + 1 reuses tile j's slot
       slot_j = (slot_j == D) ? 0 : slot_j + 1;
@@ -673,29 +687,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 // FULL[s] (IIR -> FHT) and EMPTY[s] (FHT -> IIR), so the recursions of tile j+1
 // overlap the FHT levels of tile j.
 // ===========================================================================
-// ---- TMA (cp.async.bulk.tensor) + mbarrier ----
-__device__ __forceinline__ unsigned smem_u32(int off) { return (unsigned)__cvta_generic_to_shared(sm + off); }
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned bar) {
   asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(bar), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-// 2D tile box (cols c0.., rows r0..) of the linogram -> shared memory, completing on `bar`.
-// Out-of-range columns (c0 < 0 or beyond 2N) are zero-filled by the TMA unit.
-__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int r0, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
-      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(r0), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 
@@ -1215,8 +1211,8 @@ size_t sweep_a_smem(const SweepGeom& g) {
   const int O2 = 4;
   const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : O2 + 4 * ((7 * 3) / 4);
   const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4), PL = pitch4(X + 4);
-  return ((size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4) *
-         sizeof(float);
+  return ((size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4 + 6 +
+          2) * sizeof(float);
 }
 
 size_t sweep_ws_smem(const SweepGeom& g) {
@@ -1224,6 +1220,21 @@ size_t sweep_ws_smem(const SweepGeom& g) {
   const int PF = pitch4(8 + X + 4), PS = pitch4(56 + X + 4), PL = PF;
   return ((size_t)3 * H * PF + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4 + 8 + 4) *
          sizeof(float);
+}
+
+
+
+size_t pair_b_smem(const SweepGeom& g) {
+  const int NB = g.NB, XB = g.XB;
+  int m = 0;
+  while ((1 << m) < NB) ++m;
+  const int R1 = (m >= 5) ? 3 : 2, R2 = m - R1;
+  const int O1 = (R1 == 3) ? 8 : 4;
+  const int HS = pb_halo(R1, R2);
+  const int HI = HS + O1;
+  const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
+  const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB + 4;
+  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG) * sizeof(float);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -1243,30 +1254,18 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 2D map of the linogram batch: dim0 = s (W columns), dim1 = rows (slices * 4N); box 76 x 64.
-static cudaError_t make_lin_map(CUtensorMap* m, const float* lin, int slices, const SweepGeom& g) {
+static cudaError_t make_lin_map(CUtensorMap* m, const float* lin, int slices, const SweepGeom& g, int box_w,
+                                int box_h) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
   const cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)slices * 4 * g.N};
   const cuuint64_t strides[1] = {(cuuint64_t)g.W * sizeof(float)};
-  const cuuint32_t box[2] = {(cuuint32_t)pitch4(8 + g.X + 4), 64};
+  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(lin), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
-}
-
-size_t pair_b_smem(const SweepGeom& g) {
-  const int NB = g.NB, XB = g.XB;
-  int m = 0;
-  while ((1 << m) < NB) ++m;
-  const int R1 = (m >= 5) ? 3 : 2, R2 = m - R1;
-  const int O1 = (R1 == 3) ? 8 : 4;
-  const int HS = pb_halo(R1, R2);
-  const int HI = HS + O1;
-  const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
-  const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB + 4;
-  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG) * sizeof(float);
 }
 
 template <int H, int X, bool IIR, bool BETA>
@@ -1285,9 +1284,13 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   if (per < 1) per = 1;
   const long long nitems = (long long)slices * nf * g.NB;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
+  CUtensorMap tF, tL;
+  e = make_lin_map(&tF, lin, slices, g, pitch4(8 + X + 4), H);
+  if (e == cudaSuccess) e = make_lin_map(&tL, lin, slices, g, pitch4(X + 4), H);
+  if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, counter);
+  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, counter, tF, tL);
   return cudaGetLastError();
 }
 
@@ -1307,7 +1310,7 @@ static cudaError_t launch_ws_t(const float* lin, float* R, int slices, int f0, i
   const long long nitems = (long long)slices * nf * g.NB;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
   CUtensorMap tm;
-  e = make_lin_map(&tm, lin, slices, g);
+  e = make_lin_map(&tm, lin, slices, g, pitch4(8 + g.X + 4), 64);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
@@ -1319,10 +1322,12 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
                            long long lin_slice_stride, const SweepGeom& g, const SweepIir& k,
                            bool iir, int* counter, cudaStream_t st, int* launches) {
   if (slices <= 0 || nf <= 0) return cudaSuccess;
+  // the TMA maps address rows (slice*4 + family)*N + t of a contiguous batch
+  if (f0 != 0 || nf != 4 || lin_slice_stride != 4LL * g.N * g.W || (reinterpret_cast<uintptr_t>(lin) & 15))
+    return cudaErrorInvalidValue;
   const bool beta = k.beta.x != 0.0f;
   cudaError_t e;
-  if (g.H == 64 && g.X == 64 && g.ws && f0 == 0 && nf == 4 && lin_slice_stride == 4LL * g.N * g.W &&
-      (reinterpret_cast<uintptr_t>(lin) & 15) == 0) {
+  if (g.H == 64 && g.X == 64 && g.ws) {
     if (!iir) e = launch_ws_t<false, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
     else if (beta) e = launch_ws_t<true, true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
     else e = launch_ws_t<true, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
