@@ -1038,7 +1038,8 @@ __global__ void __launch_bounds__(128, 2)
 template <int R1, int R2, int XB, int PAIR>
 __global__ void __launch_bounds__(256, 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
-             long long nitems) {
+             long long nitems, const __grid_constant__ CUtensorMap tmapR,
+             const __grid_constant__ CUtensorMap tmapI) {
   constexpr int NT = 256;
   constexpr int NB = 1 << (R1 + R2);
   constexpr int NR1 = 1 << R1, NR2 = 1 << R2;
@@ -1052,15 +1053,22 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int PI = pitch4(4 * NQF);
   constexpr int PS = pitch4(HS + XB + 4);
   constexpr int PK = PAIR == 0 ? XB + 4 : XB + 1;     // pair 1 reads park columns
-  constexpr int PG = NB + 4;                          // image staging pitch (pair 1)
+  constexpr int PG = NB;                              // image staging pitch (pair 1, TMA box)
   constexpr int oIn = 0;                              // [2 fam][NB][PI]; park aliases it
   constexpr int oS = 2 * NB * PI;                     // [2 fam][NB][PS]
   constexpr int oG = oS + 2 * NB * PS;                // [XB][PG] image rows (pair 1)
   static_assert((HS + XB) % C1 == 0 && XB % C2 == 0, "pass-B item tiling");
   static_assert(2 * NB * PK <= 2 * NB * PI, "park must fit in the input buffer");
-  const int N = g.N, H = g.H, WR = g.WR;
+  const int N = g.N, H = g.H;
   const int tid = threadIdx.x;
   const int nx = (N + XB - 1) / XB;
+  constexpr int oBar = oG + XB * PG;                  // one mbarrier (8-byte aligned)
+  if (tid == 0) {
+    mbar_init(smem_u32(oBar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph = 0;
 
   for (long long t = blockIdx.x; t < nitems; t += gridDim.x) {
     const long long per = (long long)nx * H;
@@ -1069,58 +1077,23 @@ __global__ void __launch_bounds__(256, 2)
     const int ch = rem / nx;
     const int x0 = (rem - ch * nx) * XB;
     float* out = img + sl * (long long)N * N;
-    // ---- fills: both families' compact rows (+ image rows for pair 1); lanes cover
-    //      consecutive quads of a row (whole 128-byte lines) ----
-    {
-      constexpr int nq = NQF;                            // quads per row (>= (HI+XB)/4)
-      constexpr int NROW = 2 * NB;
-      constexpr int W32 = nq / 32, TAIL = nq % 32;       // full 32-quad blocks, tail quads
-      const int lane = tid & 31, warp = tid >> 5;
-      auto row_src = [&](int rr, int& jp0, const float*& row) {
-        const int q = rr / NB, bq = rr % NB;
-        const int xs = (q == 0) ? x0 : (N - x0 - XB);
-        jp0 = xs - HI + NB;                              // compact column j' = v - N + NB
-        row = Rin + ((((sl * 4 + 2 * PAIR + q) * NB + bq) * (long long)H) + ch) * WR;
-      };
-      for (int rr = warp; rr < NROW; rr += NT / 32) {
-        int jp0;
-        const float* row;
-        row_src(rr, jp0, row);
+    // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
+    //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
+    //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
+    if (tid == 0) {
+      fence_proxy_async();
+      const unsigned bar = smem_u32(oBar);
+      mbar_expect_tx(bar, 2u * NB * PI * 4 + (PAIR == 1 ? (unsigned)XB * PG * 4 : 0u));
 #pragma unroll
-        for (int kb = 0; kb < W32; ++kb) {
-          const int jp = jp0 + 4 * (32 * kb + lane);
-          const bool ok = (jp >= 0) && (jp < WR);
-          cp16(oIn + rr * PI + 4 * (32 * kb + lane), ok ? row + jp : row, ok);
-        }
+      for (int q = 0; q < 2; ++q) {
+        const int xs = (q == 0) ? x0 : (N - x0 - XB);
+        tma_load_3d(smem_u32(oIn + q * NB * PI), &tmapR, xs - HI + NB, ch,
+                    (int)((sl * 4 + 2 * PAIR + q) * NB), bar);
       }
-      if (TAIL > 0) {
-        constexpr int RPI = 32 / TAIL > 0 ? 32 / TAIL : 1;   // rows per warp instruction
-        for (int rb = warp * RPI; rb < NROW; rb += (NT / 32) * RPI) {
-          const int rr = rb + lane / TAIL;
-          if (lane / TAIL < RPI && rr < NROW) {
-            int jp0;
-            const float* row;
-            row_src(rr, jp0, row);
-            const int qd = 32 * W32 + lane % TAIL;
-            const int jp = jp0 + 4 * qd;
-            const bool ok = (jp >= 0) && (jp < WR);
-            cp16(oIn + rr * PI + 4 * qd, ok ? row + jp : row, ok);
-          }
-        }
-      }
-      if (PAIR == 1) {
-        constexpr int gq = NB / 4;                       // quads per staged image row
-        constexpr int RPI = 32 / gq;                     // image rows per warp instruction
-        for (int i0 = warp * RPI; i0 < XB; i0 += (NT / 32) * RPI) {
-          const int i = i0 + lane / gq, qd = lane % gq;
-          const bool ok = x0 + i < N;
-          cp16(oG + i * PG + 4 * qd, out + (long long)(ok ? x0 + i : 0) * N + ch * NB + 4 * qd, ok);
-        }
-      }
-      cp_commit();
+      if (PAIR == 1) tma_load_2d(smem_u32(oG), &tmapI, ch * NB, (int)(sl * N + x0), bar);
     }
-    cp_wait<0>();
-    __syncthreads();
+    mbar_wait(smem_u32(oBar), ph);
+    ph ^= 1;
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
     {
       constexpr int nch = (HS + XB) / C1;
@@ -1233,8 +1206,8 @@ size_t pair_b_smem(const SweepGeom& g) {
   const int HS = pb_halo(R1, R2);
   const int HI = HS + O1;
   const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
-  const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB + 4;
-  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG) * sizeof(float);
+  const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB;
+  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG + 4) * sizeof(float);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -1362,7 +1335,37 @@ static cudaError_t launch_b_t(const float* R, float* img, int slices, float scal
   if (per < 1) per = 1;
   const long long nitems = (long long)((g.N + g.XB - 1) / g.XB) * g.H * slices;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
-  kern<<<(unsigned)grid, 256, smem, st>>>(R, img, g, scale, nitems);
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  // compact R viewed as [slices*4*NB][H][WR]; box = one channel's NB rows x PI columns
+  constexpr int NB = 1 << (R1 + R2);
+  constexpr int O1 = (R1 == 3) ? 8 : 4;
+  constexpr int HI = pb_halo(R1, R2) + O1;
+  constexpr int RPT = 256 / (2 * NB);
+  constexpr int NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
+  constexpr int PI = pitch4(4 * NQF);
+  CUtensorMap tR, tI;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)g.WR, (cuuint64_t)g.H, (cuuint64_t)slices * 4 * NB};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.WR * 4, (cuuint64_t)g.H * g.WR * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)PI, 1, (cuuint32_t)NB};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tR, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(R), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)slices * g.N};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.N * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)NB, (cuuint32_t)XB};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tI, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, img, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  kern<<<(unsigned)grid, 256, smem, st>>>(R, img, g, scale, nitems, tR, tI);
   return cudaGetLastError();
 }
 
