@@ -294,6 +294,8 @@ def run_fbp(args):
         per_launch_bytes = alg * slices_per_launch
         achieved = per_launch_bytes / (dom_ms / dom_n / 1e3) / 1e9
         trf = ncu_traffic(dom)
+        if trf is not None:
+            trf = trf * slices_per_launch               # per launch, like `achieved`
         shares = {k: round(v[0] / max(ms, 1e-9), 4) for k, v in ktimes.items()}
         path_bytes = 36.0 * N * N * total
         line = {
@@ -332,7 +334,7 @@ def run_fbp(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=16, help="slices per GPU per step")
     ap.add_argument("--n", type=int, default=N_HEADLINE)

@@ -411,7 +411,9 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   const Geometry& g = p->g;
   const size_t f_slice = p->fast ? 0 : (size_t)4 * g.N * g.W * sizeof(float);
   const size_t r_slice = (size_t)4 * g.NB * g.H * g.WR * sizeof(float);
-  const size_t budget = p->fast ? ((size_t)1 << 30) : ((size_t)256 << 20);
+  // fast path: the whole max_batch in one group up to 8 GiB of R (a small trailing
+  // group would leave most of the 444 sweep CTA slots idle); general path: 256 MiB
+  const size_t budget = p->fast ? ((size_t)8 << 30) : ((size_t)256 << 20);
   long long grp = (long long)(budget / (f_slice + r_slice));
   grp = std::max<long long>(1, std::min<long long>(grp, max_batch));
   grp = std::min<long long>(grp, 16383);
@@ -531,7 +533,10 @@ fbp_status fbp_reconstruct_host(const fbp_plan* cp, const float* sino, float* im
   const Geometry& g = p->g;
   const size_t lin_elems = (size_t)4 * g.N * g.W;
   const size_t img_elems = (size_t)g.N * g.N;
-  const int grp = p->group;
+  // pipeline granularity of the host path: at most 4 slices (or 512 MiB of
+  // linogram) per stage, so that copies overlap compute and staging stays small
+  const int grp = (int)std::max<size_t>(1, std::min<size_t>({(size_t)p->group, (size_t)4,
+                                                             ((size_t)512 << 20) / (lin_elems * 4)}));
   cudaError_t e;
   // Are the caller's buffers page-locked?  Then copy directly, else stage.
   auto pinned = [](const void* ptr) {

@@ -41,7 +41,7 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e
 def kind_of(name: str) -> str:
     for k, tag in (("k_iir", "iir"), ("k_fht_a", "fht_pass_a"), ("k_fht_b", "fht_pass_b"),
                    ("k_fht_pass_a", "fht_pass_a"), ("k_fht_pass_b", "fht_pass_b"),
-                   ("k_iir_fht_a", "iir_fht_a")):
+                   ("k_sweep_a", "fht_pass_a"), ("k_sweep_ws", "fht_pass_a"), ("k_pair_b", "fht_pass_b")):
         if k in name:
             return tag
     return "other"
