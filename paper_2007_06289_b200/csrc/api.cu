@@ -353,11 +353,10 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.WR = p->g.WR;
     sg.X = 4096 / sg.H;
     sg.nt = sg.W / sg.X;
-    sg.P = 0;   // look-ahead reads are a full step (~6 us) ahead of use: no extra prefetch
+    sg.P = 1;   // pass B: L2 prefetch distance in items (measured best; the sweep needs none)
+    if (const char* ev = std::getenv("FBP_PREFETCH")) sg.P = std::atoi(ev);
     sg.XB = 128;
     if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
-    sg.ws = 0;   // the warp-specialized variant (FBP_SWEEP_WS=1) measured slower than KS with TMA
-    if (const char* ev = std::getenv("FBP_SWEEP_WS")) sg.ws = std::atoi(ev);
     // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
     const int K = 1 << 16;
     std::vector<double> h(K, 0.0);

@@ -64,10 +64,9 @@ struct SweepGeom {
   int X;      // pass-A tile width (H * X = 4096)
   int nt;     // tiles per linogram row, W / X
   int D;      // look-ahead tiles for the anticausal carry (plan: tail bound)
-  int P;      // L2 prefetch distance in tiles
+  int P;      // pass-B L2 prefetch distance in items (env FBP_PREFETCH)
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
-  int ws;     // use the warp-specialized sweep where available (env FBP_SWEEP_WS=0 disables)
 };
 
 // Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at

@@ -98,6 +98,23 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
 }
 
 
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// L2 prefetch of a tensor box (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n"
+               ::"l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n"
+               ::"l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1) : "memory");
+}
+
 __device__ __forceinline__ void prefetch_line(const float* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -354,7 +371,9 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     const int fi = (int)(sfi - s * nf);
     const int f = f0 + fi;
     const float* src = lin + s * lin_slice_stride + ((long long)fi * N + (long long)b * H) * W;
-    float* dstR = Rout + (((s * 4 + f) * NB + b) * (long long)H) * WR;
+    // compact R layout [slice][family][cf][b][WR]: pass B reads, for one channel cf,
+    // the NB rows b as one contiguous box
+    float* dstR = Rout + (((s * 4 + f) * (long long)H) * NB + b) * WR;
     // First tile with an output pass B reads: every stored R column u >= N - b*H
     // depends on F at u - (H-1) >= N - (b+1)H + 1 only.  The sweep starts D tiles
     // earlier (warm-up tiles: IIR only) so that the causal carry into tile j0
@@ -430,7 +449,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     // ---- prologue ----
     {
       // L2 prefetch of the sweep's first tiles (one 128-byte line per thread per step)
-      const int je = min(nt, jst + (IIR ? D + 1 : 0) + g.P + 1);
+      const int je = min(nt, jst + (IIR ? D + 1 : 0) + 1);
       constexpr int LPR = X / 32;                       // lines per row per tile
       for (int e = tid; e < H * LPR * (je - jst); e += NT) {
         const int r = e % H, rest = e / H;
@@ -456,12 +475,6 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 
     for (int j = jst; j < nt; ++j) {
       const int oFc = oF;
-      {
-        const int jp = j + (IIR ? D + 1 : 0) + g.P + 1;
-        constexpr int LPR = X / 32;
-        if (g.P > 0 && jp < nt && tid < H * LPR)
-          prefetch_line(src + (long long)(tid % H) * W + jp * X + 32 * (tid / H));
-      }
       const int jl = j + D + 1;
 
       tma_wait(0);                                      // F tile of step j landed
@@ -635,7 +648,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           const int cf = c * NR2 + r;
           const int ulo = N - b * (cf + 1);
           const int uhi = W - cf * b;
-          float* o = dstR + (long long)cf * WR + (cf * b - N + NB);
+          float* o = dstR + (long long)cf * NB * WR + (cf * b - N + NB);
           if (ubase >= ulo && ubase + C2 <= uhi) {
 #pragma unroll
             for (int t = 0; t < C2; ++t) st_ef(o + ubase + t, col(v[r], O2 + t), pol_ef);
@@ -661,359 +674,6 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           const int cb = (rr & 7) * (rr >> 3);
           const int nq = (O2 + (cb & ~3)) / 4 + 1;
           for (int qd = tid & 1; qd < nq && qd < MAXQ; qd += 2) {
-            const int c0 = HS + 4 - 4 * (qd + 1);
-            st4(oS + rr * PS + c0, ld4(oS + rr * PS + X + c0));
-          }
-        }
-      }
-    }
-  }
-}
-
-// ===========================================================================
-// Warp-specialized sweep (H = 64, X = 64: N = 2048).  128 threads per CTA:
-//   warps 0-1, the IIR group, thread = linogram row r of the block:
-//     lands tiles (cp.async) into a 3-slot F ring, runs the two recursions of its
-//     row EXACTLY sequentially over the tile (the initial states are known: the
-//     causal state from the previous tile, the anticausal one from the look-ahead
-//     aggregates, R22), so no chunk scan and no fix-up are needed:
-//       half A: causal over [0,32) || anticausal over [63..32]   (packed f32x2)
-//       half B: causal over [32,64) || anticausal over [31..0]
-//     writes F = y+ + y- in place, then reduces look-ahead tile j + D + 1 to its
-//     anticausal aggregate (packed halves + A^32).
-//   warps 2-3, the FHT group: FHT levels 1-3 and 4-6 on 8 x 8 items of the
-//     ready slot, compact R stores.
-// The groups hand slots over with named barriers (bar.arrive / bar.sync):
-// FULL[s] (IIR -> FHT) and EMPTY[s] (FHT -> IIR), so the recursions of tile j+1
-// overlap the FHT levels of tile j.
-// ===========================================================================
-__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ void nb_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nb_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-
-// Exact packed sweep of one half: .x causal over xa[0..31] (left to right) from
-// state ca, .y anticausal over xb[31..0] (right to left) from state cb.  Feedforward
-// neighbours: causal x[-1], x[-2] = xal0, xal1; anticausal x[32], x[33] = xbr0, xbr1.
-// Returns the packed outputs (i-th: causal at i, anticausal at 31-i) and the end
-// states (causal after sample 31; anticausal after sample 0).
-template <bool BETA>
-__device__ __forceinline__ void half_sweep(const float* xa, const float* xb, float xal0, float xal1,
-                                           float xbr0, float xbr1, float2 s1, float2 s2, float2 s3,
-                                           const SweepIir& k, float2 (&yp)[32], float2& e1,
-                                           float2& e2, float2& e3) {
-  float2 dprev = make_float2(xal0 - xal1, xbr0 - xbr1);
-  float2 y1 = s1, y2 = s2, y3 = s3;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float2 d;
-    d.x = xa[i] - (i == 0 ? xal0 : xa[i - 1]);
-    d.y = xb[31 - i] - (i == 0 ? xbr0 : xb[32 - i]);
-    float2 u = __fmul2_rn(k.c1, dprev);
-    u = __ffma2_rn(k.c0, d, u);
-    if (BETA) {
-      u.x = fmaf(k.beta.x, xa[i], u.x);
-      u.y = fmaf(k.beta.x, xb[31 - i], u.y);
-    }
-    float2 v = __ffma2_rn(k.na3, y3, u);
-    v = __ffma2_rn(k.na2, y2, v);
-    v = __ffma2_rn(k.na1, y1, v);
-    y3 = y2;
-    y2 = y1;
-    y1 = v;
-    dprev = d;
-    yp[i] = v;
-  }
-  e1 = y1;
-  e2 = y2;
-  e3 = y3;
-}
-
-template <bool IIR, bool BETA>
-__global__ void __launch_bounds__(128, 2)
-    k_sweep_ws(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
-               int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter,
-               const __grid_constant__ CUtensorMap tmap) {
-  constexpr int H = 64, X = 64, NSLOT = 3;
-  constexpr int HF = 8;
-  constexpr int C8 = 8;                                  // item columns (8 x 8 items)
-  constexpr int O = It<3, C8>::O;                        // 8
-  constexpr int HS = O + 4 * ((7 * 7) / 4);              // 56: step-2 input halo
-  constexpr int PF = pitch4(HF + X + 4);                 // 76 = TMA box width
-  constexpr int PS = pitch4(HS + X + 4);                 // 124
-  constexpr int PL = PF;                                 // look-ahead slot: same box
-  constexpr int oF = 0, oS = NSLOT * H * PF, oLA = oS + H * PS, oRing = oLA + H * PL;
-  constexpr unsigned BOX_BYTES = H * PF * 4;
-  enum { BAR_IIR = 1, BAR_FHT = 2, BAR_FULL = 3, BAR_EMPTY = 3 + NSLOT };
-
-  const int tid = threadIdx.x;
-  const int D = g.D;
-  const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;      // 4 mbarriers (8-byte aligned)
-  int* s_item = reinterpret_cast<int*>(sm + oBar + 8);
-  // mbarriers: 0..2 = F slots, 3 = look-ahead slot
-  if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  unsigned ph = 0;                                        // phase bits of the 4 mbarriers (IIR group)
-  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
-  const long long nsf = (long long)slices * nf;
-  const long long nitems = nsf * NB;
-  const bool is_iir = tid < 64;
-  const int lt = tid & 63;                                // thread index within the group
-  const int lane = tid & 31, gw = (tid >> 5) & 1;          // warp index within the group
-  const unsigned long long pol_ef = policy_evict_first();
-
-  while (true) {
-    __syncthreads();
-    if (tid == 0) *s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    const long long item = *s_item;
-    if (item >= nitems) break;
-    const int b = NB - 1 - (int)(item / nsf);            // longest sweeps first
-    const long long sfi = item - (long long)(NB - 1 - b) * nsf;
-    const long long s = sfi / nf;
-    const int fi = (int)(sfi - s * nf);
-    const int f = f0 + fi;
-    const float* src = lin + s * lin_slice_stride + ((long long)fi * N + (long long)b * H) * W;
-    const int trow = (int)((s * 4 + fi) * N + (long long)b * H);   // TMA row of the block (stride 4NW)
-    const int j0 = (N - (b + 1) * H + 1) / X;
-    const int jst = IIR ? max(0, j0 - D) : j0;
-
-    if (is_iir) {
-      // =========================== IIR group ===========================
-      const int r = lt;
-      // TMA landings: one box of 64 rows x 76 columns per tile, issued by thread 0.
-      //   F slot: columns [jt*X - 8, jt*X + 68): halo room, left neighbour quad, core,
-      //           right neighbour quad; look-ahead: columns [jt*X, jt*X + 76).
-      // Waiters track the phase of each mbarrier (bit i of ph).
-      auto land = [&](int jt, int slot) {
-        if (jt < nt && r == 0) {
-          fence_proxy_async();
-          const unsigned bar = smem_u32(oBar + 2 * slot);
-          mbar_expect_tx(bar, BOX_BYTES);
-          tma_load_2d(smem_u32(oF + slot * H * PF), &tmap, jt * X - 8, trow, bar);
-        }
-      };
-      auto land_wait = [&](int jt, int slot) {
-        if (jt < nt) {
-          mbar_wait(smem_u32(oBar + 2 * slot), (ph >> slot) & 1);
-          ph ^= 1u << slot;
-        }
-      };
-      auto la_land = [&](int ob, int bar_i, int jt) {
-        if (jt < nt && r == 0) {
-          fence_proxy_async();
-          const unsigned bar = smem_u32(oBar + 2 * bar_i);
-          mbar_expect_tx(bar, BOX_BYTES);
-          tma_load_2d(smem_u32(ob), &tmap, jt * X, trow, bar);
-        }
-      };
-      // anticausal zero-state aggregate of landed tile jt (own row) -> ring slot
-      auto la_finish = [&](int ob, int pl, int jt, int slot) {
-        float lx[66];
-        const int rowL = ob + r * pl;
-#pragma unroll
-        for (int q = 0; q < 17; ++q) {
-          const float4 v = ld4(rowL + 4 * q);
-          if (4 * q < 66) lx[4 * q] = v.x;
-          if (4 * q + 1 < 66) lx[4 * q + 1] = v.y;
-          if (4 * q + 2 < 66) lx[4 * q + 2] = v.z;
-          if (4 * q + 3 < 66) lx[4 * q + 3] = v.w;
-        }
-        float va[3], hi[3];
-        {
-          float t0[3];
-          chunk_anticausal_state<BETA>(*reinterpret_cast<const float(*)[32]>(lx), lx[32], lx[33], k, t0);
-          chunk_anticausal_state<BETA>(*reinterpret_cast<const float(*)[32]>(lx + 32), lx[64], lx[65], k, hi);
-          va[0] = t0[0];
-          va[1] = t0[1];
-          va[2] = t0[2];
-        }
-        mv1(k.M1, hi, va);                                // state at 0 = lo + A^32 hi
-        const bool live = jt < nt;
-        const int o = oRing + (slot * H + r) * 3;
-        sm[o] = live ? va[0] : 0.f;
-        sm[o + 1] = live ? va[1] : 0.f;
-        sm[o + 2] = live ? va[2] : 0.f;
-      };
-
-      float hal[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) hal[q] = 0.f;
-      float2 cin1 = make_float2(0.f, 0.f), cin2 = cin1, cin3 = cin1;   // causal state (.x)
-      land(jst, 0);
-      if (IIR) {
-        // prologue look-ahead (tiles jst+1 .. jst+D) through the LA slot and slots 1, 2
-        for (int i0 = 1; i0 <= D; i0 += 3) {
-          const int nb = min(3, D - i0 + 1);
-          for (int k2 = 0; k2 < nb; ++k2)
-            la_land(k2 == 0 ? oLA : oF + k2 * H * PF, k2 == 0 ? 3 : k2, jst + i0 + k2);
-          for (int k2 = 0; k2 < nb; ++k2) {
-            const int bi = k2 == 0 ? 3 : k2;
-            land_wait(jst + i0 + k2, bi);
-            la_finish(k2 == 0 ? oLA : oF + k2 * H * PF, PF, jst + i0 + k2, i0 + k2);
-          }
-          nb_sync(BAR_IIR, 64);                           // buffers free before reuse
-        }
-      }
-      int slot_j = 0;                                     // ring slot of tile j
-      for (int j = jst; j < nt; ++j) {
-        const int sl = (j - jst) % NSLOT;
-        const int sn = (sl + 1 == NSLOT) ? 0 : sl + 1;    // slot of tile j + 1
-        // tile j + 1 -> slot sn, free once the FHT group released tile j - 2
-        if (j - 2 >= jst) nb_sync(BAR_EMPTY + sn, 128);
-        if (IIR) la_land(oLA, 3, j + D + 1);
-        land(j + 1, sn);
-        land_wait(j, sl);                                 // tile j is in slot sl
-        const int rowF = oF + sl * H * PF + r * PF;
-        if (IIR) {
-          float x[68];                                    // x[i] = sample i - 2 (cols -2..65)
-#pragma unroll
-          for (int q = 0; q < 17; ++q) {
-            const float4 v = ld4(rowF + HF - 4 + 4 * q + 0);
-            if (q == 0) {
-              x[0] = v.z;
-              x[1] = v.w;
-            } else {
-              x[4 * q - 2] = v.x;
-              x[4 * q - 1] = v.y;
-              x[4 * q] = v.z;
-              x[4 * q + 1] = v.w;
-            }
-          }
-          {
-            const float4 v = ld4(rowF + HF + X);
-            x[66] = v.x;
-            x[67] = v.y;
-          }
-          // anticausal carry into this tile's right edge (Horner over the ring)
-          float tm[3];
-          {
-            int rs = slot_j + D;
-            if (rs > D) rs -= D + 1;
-            tm[0] = sm[oRing + (rs * H + r) * 3];
-            tm[1] = sm[oRing + (rs * H + r) * 3 + 1];
-            tm[2] = sm[oRing + (rs * H + r) * 3 + 2];
-            for (int i = D - 1; i >= 1; --i) {
-              rs = (rs == 0) ? D : rs - 1;
-              float acc[3] = {sm[oRing + (rs * H + r) * 3], sm[oRing + (rs * H + r) * 3 + 1],
-                              sm[oRing + (rs * H + r) * 3 + 2]};
-              mv1(k.MX, tm, acc);
-              tm[0] = acc[0];
-              tm[1] = acc[1];
-              tm[2] = acc[2];
-            }
-          }
-          const float* xs = x + 2;                        // xs[i] = sample i
-          float2 ya[32], yb[32], e1, e2, e3;
-          // half A: causal [0,32) from cin, anticausal [63..32] from tm
-          half_sweep<BETA>(xs, xs + 32, xs[-1], xs[-2], xs[64], xs[65],
-                           make_float2(cin1.x, tm[0]), make_float2(cin2.x, tm[1]),
-                           make_float2(cin3.x, tm[2]), k, ya, e1, e2, e3);
-          // half B: causal [32,64) from A's causal end, anticausal [31..0] from A's end
-          float2 f1, f2, f3;
-          half_sweep<BETA>(xs + 32, xs, xs[31], xs[30], xs[32], xs[33], e1, e2, e3, k, yb, f1, f2, f3);
-          cin1 = f1;
-          cin2 = f2;
-          cin3 = f3;
-          // F[i] = y+[i] + y-[i]:  i < 32: ya[i].x + yb[31-i].y;  i >= 32: yb[i-32].x + ya[63-i].y
-          st4(rowF, make_float4(hal[0], hal[1], hal[2], hal[3]));
-          st4(rowF + 4, make_float4(hal[4], hal[5], hal[6], hal[7]));
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int i = 4 * q;
-            st4(rowF + HF + i, make_float4(ya[i].x + yb[31 - i].y, ya[i + 1].x + yb[30 - i].y,
-                                           ya[i + 2].x + yb[29 - i].y, ya[i + 3].x + yb[28 - i].y));
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int i = 4 * q;
-            st4(rowF + HF + 32 + i, make_float4(yb[i].x + ya[31 - i].y, yb[i + 1].x + ya[30 - i].y,
-                                                yb[i + 2].x + ya[29 - i].y, yb[i + 3].x + ya[28 - i].y));
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) hal[q] = yb[24 + q].x + ya[7 - q].y;   // F[56 + q]
-        } else {
-          float4 a = ld4(rowF + HF + X - 8), c = ld4(rowF + HF + X - 4);
-          st4(rowF, make_float4(hal[0], hal[1], hal[2], hal[3]));
-          st4(rowF + 4, make_float4(hal[4], hal[5], hal[6], hal[7]));
-          hal[0] = a.x; hal[1] = a.y; hal[2] = a.z; hal[3] = a.w;
-          hal[4] = c.x; hal[5] = c.y; hal[6] = c.z; hal[7] = c.w;
-        }
-        fence_proxy_async();                              // generic F writes before the slot's next TMA
-        nb_arrive(BAR_FULL + sl, 128);                    // slot sl holds F of tile j
-        if (IIR) {
-          land_wait(j + D + 1, 3);
-          la_finish(oLA, PL, j + D + 1, slot_j);          // tile j + D + 1 reuses tile j's slot
-          nb_sync(BAR_IIR, 64);                           // LA slot free for the next landing
-        }
-        slot_j = (slot_j == D) ? 0 : slot_j + 1;
-      }
-      // consume the FHT group's last releases (tiles nt-2, nt-1)
-      for (int jj = max(jst, nt - 2); jj < nt; ++jj) nb_sync(BAR_EMPTY + (jj - jst) % NSLOT, 128);
-    } else {
-      // =========================== FHT group ===========================
-      float* dstR = Rout + (((s * 4 + f) * NB + b) * (long long)H) * WR;
-      const int G = lt >> 3, jj = lt & 7;                // step-1 item: rows 8G.., cols 8jj..
-      const int c = lt >> 3;                              // step-2 item: channel c, cols 8jj..
-      for (int j = jst; j < nt; ++j) {
-        const int sl = (j - jst) % NSLOT;
-        nb_sync(BAR_FULL + sl, 128);
-        if (j >= j0) {
-          float2 v[8][It<3, C8>::T / 2];
-          item_load<3, C8>(oF + sl * H * PF + (G * 8) * PF + C8 * jj, PF, 0, v);   // HF + 8jj - 8
-          item_fht<3, C8>(v);
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            const int o = oS + (G * 8 + rr) * PS + HS + C8 * jj + ((rr * G) & 3);
-#pragma unroll
-            for (int t = 0; t < C8; ++t) sm[o + t] = col(v[rr], O + t);
-          }
-        }
-        nb_arrive(BAR_EMPTY + sl, 128);                  // slot sl may be refilled
-        nb_sync(BAR_FHT, 64);
-        if (j >= j0) {
-          float2 v[8][It<3, C8>::T / 2];
-          item_load<3, C8>(oS + c * PS + HS + C8 * jj - O, 8 * PS, c, v);
-          item_fht<3, C8>(v);
-          const int ubase = j * X + C8 * jj;
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) {
-            const int cf = c * 8 + rr;
-            const int ulo = N - b * (cf + 1);
-            const int uhi = W - cf * b;
-            float* o = dstR + (long long)cf * WR + (cf * b - N + NB);
-            if (ubase >= ulo && ubase + C8 <= uhi) {
-#pragma unroll
-              for (int t = 0; t < C8; ++t) st_ef(o + ubase + t, col(v[rr], O + t), pol_ef);
-            } else if (ubase + C8 > ulo && ubase < uhi) {
-#pragma unroll
-              for (int t = 0; t < C8; ++t) {
-                const int u = ubase + t;
-                if (u >= ulo && u < uhi) st_ef(o + u, col(v[rr], O + t), pol_ef);
-              }
-            }
-          }
-        }
-        nb_sync(BAR_FHT, 64);
-        if (j >= j0) {
-          // S1 halo for the next tile: row (b', c') reads virtual columns >= HS - O - c'b'
-          const int rr = lt;
-          const int cb = (rr & 7) * (rr >> 3);
-          const int nq = (O + (cb & ~3)) / 4 + 1;
-          for (int qd = 0; qd < nq; ++qd) {
             const int c0 = HS + 4 - 4 * (qd + 1);
             st4(oS + rr * PS + c0, ld4(oS + rr * PS + X + c0));
           }
@@ -1080,6 +740,24 @@ __global__ void __launch_bounds__(256, 2)
     // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
     //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
     //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
+    if (tid == 0 && g.P > 0) {
+      // L2 prefetch of the boxes of item t + P*gridDim.x (hides the HBM latency of
+      // the compact R rows behind this and the next items)
+      const long long tp = t + (long long)g.P * gridDim.x;
+      if (tp < nitems) {
+        const long long per2 = (long long)nx * H;
+        const long long sl2 = tp / per2;
+        const int rem2 = (int)(tp - sl2 * per2);
+        const int ch2 = rem2 / nx;
+        const int x02 = (rem2 - ch2 * nx) * XB;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int xs = (q == 0) ? x02 : (N - x02 - XB);
+          tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (int)((sl2 * 4 + 2 * PAIR + q) * H + ch2));
+        }
+        if (PAIR == 1) tma_prefetch_2d(&tmapI, ch2 * NB, (int)(sl2 * N + x02));
+      }
+    }
     if (tid == 0) {
       fence_proxy_async();
       const unsigned bar = smem_u32(oBar);
@@ -1087,8 +765,8 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int xs = (q == 0) ? x0 : (N - x0 - XB);
-        tma_load_3d(smem_u32(oIn + q * NB * PI), &tmapR, xs - HI + NB, ch,
-                    (int)((sl * 4 + 2 * PAIR + q) * NB), bar);
+        tma_load_3d(smem_u32(oIn + q * NB * PI), &tmapR, xs - HI + NB, 0,
+                    (int)((sl * 4 + 2 * PAIR + q) * H + ch), bar);
       }
       if (PAIR == 1) tma_load_2d(smem_u32(oG), &tmapI, ch * NB, (int)(sl * N + x0), bar);
     }
@@ -1188,15 +866,6 @@ size_t sweep_a_smem(const SweepGeom& g) {
           2) * sizeof(float);
 }
 
-size_t sweep_ws_smem(const SweepGeom& g) {
-  const int H = 64, X = 64;
-  const int PF = pitch4(8 + X + 4), PS = pitch4(56 + X + 4), PL = PF;
-  return ((size_t)3 * H * PF + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4 + 8 + 4) *
-         sizeof(float);
-}
-
-
-
 size_t pair_b_smem(const SweepGeom& g) {
   const int NB = g.NB, XB = g.XB;
   int m = 0;
@@ -1267,30 +936,6 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   return cudaGetLastError();
 }
 
-template <bool IIR, bool BETA>
-static cudaError_t launch_ws_t(const float* lin, float* R, int slices, int f0, int nf, long long stride,
-                               const SweepGeom& g, const SweepIir& k, int* counter, cudaStream_t st) {
-  auto kern = k_sweep_ws<IIR, BETA>;
-  const size_t smem = sweep_ws_smem(g);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
-  if (g.ctas_a > 0 && g.ctas_a < per) per = g.ctas_a;
-  if (per < 1) per = 1;
-  const long long nitems = (long long)slices * nf * g.NB;
-  const long long grid = std::min<long long>(nitems, (long long)sms * per);
-  CUtensorMap tm;
-  e = make_lin_map(&tm, lin, slices, g, pitch4(8 + g.X + 4), 64);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, 128, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, counter, tm);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int nf,
                            long long lin_slice_stride, const SweepGeom& g, const SweepIir& k,
                            bool iir, int* counter, cudaStream_t st, int* launches) {
@@ -1300,13 +945,6 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
     return cudaErrorInvalidValue;
   const bool beta = k.beta.x != 0.0f;
   cudaError_t e;
-  if (g.H == 64 && g.X == 64 && g.ws) {
-    if (!iir) e = launch_ws_t<false, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
-    else if (beta) e = launch_ws_t<true, true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
-    else e = launch_ws_t<true, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st);
-    if (launches) ++*launches;
-    return e;
-  }
 #define FBP_SWEEP_CASE(HH, XX)                                                                     \
   if (g.H == HH) {                                                                                 \
     if (!iir) e = launch_a_t<HH, XX, false, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
@@ -1337,7 +975,7 @@ static cudaError_t launch_b_t(const float* R, float* img, int slices, float scal
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
   EncodeTiledFn enc = encode_fn();
   if (!enc) return cudaErrorNotSupported;
-  // compact R viewed as [slices*4*NB][H][WR]; box = one channel's NB rows x PI columns
+  // compact R viewed as [slices*4*H][NB][WR]; box = one channel's NB rows x PI columns
   constexpr int NB = 1 << (R1 + R2);
   constexpr int O1 = (R1 == 3) ? 8 : 4;
   constexpr int HI = pb_halo(R1, R2) + O1;
@@ -1346,9 +984,9 @@ static cudaError_t launch_b_t(const float* R, float* img, int slices, float scal
   constexpr int PI = pitch4(4 * NQF);
   CUtensorMap tR, tI;
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)g.WR, (cuuint64_t)g.H, (cuuint64_t)slices * 4 * NB};
-    const cuuint64_t strides[2] = {(cuuint64_t)g.WR * 4, (cuuint64_t)g.H * g.WR * 4};
-    const cuuint32_t box[3] = {(cuuint32_t)PI, 1, (cuuint32_t)NB};
+    const cuuint64_t dims[3] = {(cuuint64_t)g.WR, (cuuint64_t)NB, (cuuint64_t)slices * 4 * g.H};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.WR * 4, (cuuint64_t)NB * g.WR * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)PI, (cuuint32_t)NB, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     if (enc(&tR, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(R), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
