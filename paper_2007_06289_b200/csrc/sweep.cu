@@ -18,9 +18,8 @@
 // state at the left edge of tile t produced by the inputs inside tile t; tiles
 // beyond j + D are dropped, and D is chosen by the plan so that the dropped tail
 // of the impulse response is below 1e-12 of its l1 norm (R22).  The
-// look-ahead tiles are read one tile ahead with plain loads (an L2 prefetch issued
-// P tiles earlier brings them on chip); each tile is later landed a second time
-// (L2 hit) for the exact local pass.
+// look-ahead tile is landed by TMA at the start of a step and reduced at its end;
+// each tile is landed a second time (L2 hit) when it becomes the current tile.
 //
 // FHT items.  A radix-2^R step after l levels computes, for 2^R consecutive
 // blocks of 2^l rows and one channel c (PAPER.md recursion):
@@ -47,17 +46,6 @@ extern __shared__ float sm[];
 __device__ __forceinline__ float4 ld4(int off) { return *reinterpret_cast<const float4*>(sm + off); }
 __device__ __forceinline__ void st4(int off, float4 v) { *reinterpret_cast<float4*>(sm + off) = v; }
 
-__device__ __forceinline__ void cp16(int soff, const float* g, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sm + soff);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 16 : 0));
-}
-// cp.async with an L2 cache policy (createpolicy): second reads of linogram tiles
-// are marked evict-first so that they do not displace tiles still ahead.
-__device__ __forceinline__ void cp16h(int soff, const float* g, bool valid, unsigned long long pol) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sm + soff);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(g),
-               "r"(valid ? 16 : 0), "l"(pol));
-}
 __device__ __forceinline__ unsigned long long policy_evict_first() {
   unsigned long long p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
@@ -67,10 +55,6 @@ __device__ __forceinline__ unsigned long long policy_evict_first() {
 __device__ __forceinline__ void st_ef(float* g, float v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(g), "f"(v), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int NLEFT>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT)); }
-
 // ---- TMA (cp.async.bulk.tensor) + mbarrier ----
 __device__ __forceinline__ unsigned smem_u32(int off) { return (unsigned)__cvta_generic_to_shared(sm + off); }
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -304,9 +288,6 @@ __device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], flo
   mv1(k.M16, hi, va);
 }
 
-__device__ __forceinline__ float2 shfl_up2(float2 v, int d) {
-  return make_float2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
-}
 
 }  // namespace
 
@@ -636,7 +617,13 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       __syncthreads();
       if (j + 1 < nt) land(j + 1);                       // F is free: step 1 has read it
       // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
-      if (j >= j0) {
+      // Items whose NR2 channels cf = c*NR2 + r need none of their columns (u outside
+      // [N - b(cf+1), 2N - cf*b) for every r) are skipped: up to half of them for
+      // the high blocks b.
+      constexpr int NCH2 = X / C2;
+      const int ub2 = j * X + C2 * (tid % NCH2), c2 = tid / NCH2;
+      const bool need2 = (ub2 + C2 > N - b * (c2 * NR2 + NR2)) && (ub2 < W - c2 * NR2 * b);
+      if (j >= j0 && need2) {
         constexpr int NCH = X / C2;
         const int jj = tid % NCH, c = tid / NCH;
         float2 v[NR2][It<R2, C2>::T / 2];
