@@ -219,3 +219,71 @@ def test_zero_input(fbp):
     plan = fbp.Plan(N, b, a)
     img = plan.reconstruct(torch.zeros((1, 4, N, 2 * N), device="cuda"))
     assert torch.count_nonzero(img) == 0
+
+
+# ------------------------------------------------------------ fast-path schedule
+def _tail_lookahead(b, a, X, Dmax=16):
+    """Look-ahead tiles D of reading R22, recomputed here in float64."""
+    K = 1 << 16
+    h = np.zeros(K)
+    for i in range(K):
+        v = b[i] if i < len(b) else 0.0
+        for k in range(1, len(a) + 1):
+            if i - k >= 0:
+                v -= a[k - 1] * h[i - k]
+        h[i] = v
+    tail = np.cumsum(np.abs(h)[::-1])[::-1]
+    for d in range(1, Dmax + 1):
+        if tail[max(0, d * X - 2)] <= 1e-12 * tail[0]:
+            return d
+    return 0
+
+
+@pytest.mark.parametrize("N,variant", [(512, "dc0"), (1024, "spec"), (2048, "dc0"), (2048, "spec")])
+def test_plan_path_fast(fbp, N, variant):
+    b, a = coeffs(N, variant)
+    p = fbp.Plan(N, b, a, max_batch=1).path()
+    X = 64 if N == 2048 else 128
+    assert p["fast"] and p["tile_width"] == X
+    assert p["lookahead_tiles"] == _tail_lookahead(b, a, X)
+
+
+@pytest.mark.parametrize("N", [256, 4096])
+def test_plan_path_general(fbp, N):
+    b, a = coeffs(N)
+    assert not fbp.Plan(N, b, a, max_batch=1).path()["fast"]
+    # a zero-padded 4th tap is the same filter but leaves the fast path's M, Q <= 3
+    assert not fbp.Plan(512, b + [0.0], a + [0.0], max_batch=1).path()["fast"]
+
+
+@pytest.mark.parametrize("N,cfg", [(512, 2), (2048, 3)])
+def test_fast_path_matches_general_path(fbp, N, cfg):
+    """The fused sweep (truncated carries, R22) and the exact general path are two
+    independent implementations of the same filter; they agree to fp32 rounding."""
+    b, a = coeffs(N)
+    fast = fbp.Plan(N, b, a, max_batch=2)
+    exact = fbp.Plan(N, b + [0.0], a + [0.0], max_batch=2)
+    assert fast.path()["fast"] and not exact.path()["fast"]
+    S = P.make_batch(cfg, 2, device="cuda")
+    i1 = fast.reconstruct(S).cpu().numpy()
+    i2 = exact.reconstruct(S).cpu().numpy()
+    for i in range(2):
+        assert rel_err(i1[i], i2[i]) < 1e-5
+    lin = P.integer_linogram(N, 2, seed=9).cuda()
+    assert torch.equal(fast.backproject(lin, scale=1.0), exact.backproject(lin, scale=1.0))
+
+
+def test_fast_path_determinism_host_and_composition(fbp):
+    N = 512
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=3)
+    assert plan.path()["fast"]
+    S = P.make_batch(2, 3)
+    d1 = plan.reconstruct(S.cuda()).cpu()
+    d2 = plan.reconstruct(S.cuda()).cpu()
+    assert torch.equal(d1, d2)
+    h = plan.reconstruct_host(S.numpy())
+    assert np.array_equal(h, d1.numpy())
+    F = plan.iir_filter(S.cuda())
+    bp = plan.backproject(F, scale=1.0 / N).cpu()
+    assert rel_err(bp.numpy(), d1.numpy()) < 1e-5
