@@ -30,4 +30,12 @@ for name, fn in (("reconstruct", lambda: plan.reconstruct(S, out=img)),
         fn()
     kt = plan.kernel_times()
     plan.profile(False)
-    print(name, {k: round(v[0] / 5, 4) for k, v in kt.items()}, "ms per call of", B, "slices", flush=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(10):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    print(name, {k: round(v[0] / 5, 4) for k, v in kt.items()}, "ms per call of", B, "slices;",
+          "wall %.4f ms" % (e0.elapsed_time(e1) / 10), flush=True)
