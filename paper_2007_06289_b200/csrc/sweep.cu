@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 // For PAIR 1 the image rows are staged into shared memory by cp.async while
 // the FHT steps run.  Two CTAs per SM; no cross-item prefetch.
 // ===========================================================================
-template <int R1, int R2, int XB, int PAIR>
+template <int R1, int R2, int XB, int PAIR, bool DB>
 __global__ void __launch_bounds__(256, 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
              long long nitems, const __grid_constant__ CUtensorMap tmapR,
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int NB = 1 << (R1 + R2);
   constexpr int NR1 = 1 << R1, NR2 = 1 << R2;
   constexpr int C1 = (R1 == 3) ? 4 : 8;
-  constexpr int C2 = (R2 == 3) ? 4 : 8;
+  constexpr int C2 = (R2 == 3 || XB <= 64) ? 4 : 8;
   constexpr int O1 = It<R1, C1>::O, O2 = It<R2, C2>::O;
   constexpr int HS = pb_halo(R1, R2);
   constexpr int HI = HS + O1;
@@ -701,21 +701,64 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int PS = pitch4(HS + XB + 4);
   constexpr int PK = PAIR == 0 ? XB + 4 : XB + 1;     // pair 1 reads park columns
   constexpr int PG = NB;                              // image staging pitch (pair 1, TMA box)
-  constexpr int oIn = 0;                              // [2 fam][NB][PI]; park aliases it
-  constexpr int oS = 2 * NB * PI;                     // [2 fam][NB][PS]
-  constexpr int oG = oS + 2 * NB * PS;                // [XB][PG] image rows (pair 1)
+  // DB: two input (and staging) buffers, the next item's TMA boxes land while this
+  // item computes
+  constexpr int NBUF = DB ? 2 : 1;
+  constexpr int IN_SZ = 2 * NB * PI, G_SZ = XB * PG;
+  constexpr int oIn0 = 0;                             // [NBUF][2 fam][NB][PI]; park aliases it
+  constexpr int oS = NBUF * IN_SZ;                    // [2 fam][NB][PS]
+  constexpr int oG0 = oS + 2 * NB * PS;               // [NBUF][XB][PG] image rows (pair 1)
   static_assert((HS + XB) % C1 == 0 && XB % C2 == 0, "pass-B item tiling");
   static_assert(2 * NB * PK <= 2 * NB * PI, "park must fit in the input buffer");
   const int N = g.N, H = g.H;
   const int tid = threadIdx.x;
   const int nx = (N + XB - 1) / XB;
-  constexpr int oBar = oG + XB * PG;                  // one mbarrier (8-byte aligned)
+  constexpr int oBar = oG0 + NBUF * G_SZ;             // NBUF mbarriers (8-byte aligned)
   if (tid == 0) {
-    mbar_init(smem_u32(oBar), 1);
+    for (int i = 0; i < NBUF; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   unsigned ph = 0;
+  // TMA fills of item tt into buffer bb (thread 0): both families' NB compact rows
+  // of channel ch (3D box PI x NB x 1, columns j' = xs - HI + NB.., zero-filled
+  // outside the row), for pair 1 the XB image rows x0.. (2D box NB x XB); plus an
+  // L2 prefetch of the boxes of item tt + P*gridDim.x
+  auto issue = [&](long long tt, int bb) {
+    if (tid != 0 || tt >= nitems) return;
+    const long long per2 = (long long)nx * H;
+    if (g.P > 0) {
+      const long long tp = tt + (long long)g.P * gridDim.x;
+      if (tp < nitems) {
+        const long long slp = tp / per2;
+        const int remp = (int)(tp - slp * per2);
+        const int chp = remp / nx;
+        const int x0p = (remp - chp * nx) * XB;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int xs = (q == 0) ? x0p : (N - x0p - XB);
+          tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (int)((slp * 4 + 2 * PAIR + q) * H + chp));
+        }
+        if (PAIR == 1) tma_prefetch_2d(&tmapI, chp * NB, (int)(slp * N + x0p));
+      }
+    }
+    const long long sl2 = tt / per2;
+    const int rem2 = (int)(tt - sl2 * per2);
+    const int ch2 = rem2 / nx;
+    const int x02 = (rem2 - ch2 * nx) * XB;
+    fence_proxy_async();
+    const unsigned bar = smem_u32(oBar + 2 * bb);
+    mbar_expect_tx(bar, 2u * NB * PI * 4 + (PAIR == 1 ? (unsigned)XB * PG * 4 : 0u));
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int xs = (q == 0) ? x02 : (N - x02 - XB);
+      tma_load_3d(smem_u32(oIn0 + bb * IN_SZ + q * NB * PI), &tmapR, xs - HI + NB, 0,
+                  (int)((sl2 * 4 + 2 * PAIR + q) * H + ch2), bar);
+    }
+    if (PAIR == 1) tma_load_2d(smem_u32(oG0 + bb * G_SZ), &tmapI, ch2 * NB, (int)(sl2 * N + x02), bar);
+  };
+  issue(blockIdx.x, 0);
+  int bb = 0;
 
   for (long long t = blockIdx.x; t < nitems; t += gridDim.x) {
     const long long per = (long long)nx * H;
@@ -724,41 +767,13 @@ __global__ void __launch_bounds__(256, 2)
     const int ch = rem / nx;
     const int x0 = (rem - ch * nx) * XB;
     float* out = img + sl * (long long)N * N;
+    const int oIn = oIn0 + bb * IN_SZ, oG = oG0 + bb * G_SZ;
+    if (DB) issue(t + gridDim.x, bb ^ 1);               // buffer freed by the previous item
     // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
     //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
     //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
-    if (tid == 0 && g.P > 0) {
-      // L2 prefetch of the boxes of item t + P*gridDim.x (hides the HBM latency of
-      // the compact R rows behind this and the next items)
-      const long long tp = t + (long long)g.P * gridDim.x;
-      if (tp < nitems) {
-        const long long per2 = (long long)nx * H;
-        const long long sl2 = tp / per2;
-        const int rem2 = (int)(tp - sl2 * per2);
-        const int ch2 = rem2 / nx;
-        const int x02 = (rem2 - ch2 * nx) * XB;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int xs = (q == 0) ? x02 : (N - x02 - XB);
-          tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (int)((sl2 * 4 + 2 * PAIR + q) * H + ch2));
-        }
-        if (PAIR == 1) tma_prefetch_2d(&tmapI, ch2 * NB, (int)(sl2 * N + x02));
-      }
-    }
-    if (tid == 0) {
-      fence_proxy_async();
-      const unsigned bar = smem_u32(oBar);
-      mbar_expect_tx(bar, 2u * NB * PI * 4 + (PAIR == 1 ? (unsigned)XB * PG * 4 : 0u));
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int xs = (q == 0) ? x0 : (N - x0 - XB);
-        tma_load_3d(smem_u32(oIn + q * NB * PI), &tmapR, xs - HI + NB, 0,
-                    (int)((sl * 4 + 2 * PAIR + q) * H + ch), bar);
-      }
-      if (PAIR == 1) tma_load_2d(smem_u32(oG), &tmapI, ch * NB, (int)(sl * N + x0), bar);
-    }
-    mbar_wait(smem_u32(oBar), ph);
-    ph ^= 1;
+    mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);
+    ph ^= 1u << bb;
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
     {
       constexpr int nch = (HS + XB) / C1;
@@ -837,6 +852,8 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
     __syncthreads();                                   // park / staging reused by the next item
+    if (!DB) issue(t + gridDim.x, 0);
+    if (DB) bb ^= 1;
   }
 }
 
@@ -854,6 +871,7 @@ size_t sweep_a_smem(const SweepGeom& g) {
 }
 
 size_t pair_b_smem(const SweepGeom& g) {
+  const bool db = g.XB <= 64;
   const int NB = g.NB, XB = g.XB;
   int m = 0;
   while ((1 << m) < NB) ++m;
@@ -863,7 +881,8 @@ size_t pair_b_smem(const SweepGeom& g) {
   const int HI = HS + O1;
   const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
   const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB;
-  return ((size_t)2 * NB * PI + (size_t)2 * NB * PS + (size_t)XB * PG + 4) * sizeof(float);
+  const size_t nbuf = db ? 2 : 1;
+  return (nbuf * 2 * NB * PI + (size_t)2 * NB * PS + nbuf * XB * PG + 4) * sizeof(float);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -949,7 +968,7 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
 template <int R1, int R2, int XB, int PAIR>
 static cudaError_t launch_b_t(const float* R, float* img, int slices, float scale,
                               const SweepGeom& g, cudaStream_t st) {
-  auto kern = k_pair_b<R1, R2, XB, PAIR>;
+  auto kern = k_pair_b<R1, R2, XB, PAIR, (XB <= 64)>;
   const size_t smem = pair_b_smem(g);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -998,13 +1017,13 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
                           const SweepGeom& g, cudaStream_t st, int* launches) {
   if (slices <= 0) return cudaSuccess;
   cudaError_t e = cudaErrorInvalidValue;
-  if (g.XB != 128) return e;
-#define FBP_PAIR_CASE(NBV, R1, R2)                                                          \
-  if (g.NB == NBV)                                                                          \
-    e = pair == 0 ? launch_b_t<R1, R2, 128, 0>(R, img, slices, scale, g, st)                \
-                  : launch_b_t<R1, R2, 128, 1>(R, img, slices, scale, g, st);
-  FBP_PAIR_CASE(16, 2, 2)
-  FBP_PAIR_CASE(32, 3, 2)
+#define FBP_PAIR_CASE(NBV, R1, R2, XBV)                                                     \
+  if (g.NB == NBV && g.XB == XBV)                                                           \
+    e = pair == 0 ? launch_b_t<R1, R2, XBV, 0>(R, img, slices, scale, g, st)                \
+                  : launch_b_t<R1, R2, XBV, 1>(R, img, slices, scale, g, st);
+  FBP_PAIR_CASE(16, 2, 2, 128)
+  FBP_PAIR_CASE(32, 3, 2, 128)
+  FBP_PAIR_CASE(32, 3, 2, 64)
 #undef FBP_PAIR_CASE
   if (launches) ++*launches;
   return e;
