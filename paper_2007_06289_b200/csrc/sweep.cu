@@ -458,9 +458,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       const int oFc = oF;
       const int jl = j + D + 1;
 
-      tma_wait(0);                                      // F tile of step j landed
-      __syncthreads();                                  // previous step's look-ahead reads done
-      if (IIR) la_land(oLA, PL, jl, 1);                 // consumed at the end of this step
+      tma_wait(0);                                      // F tile of step j landed (each thread)
 
       if (IIR) {
         // ---- local sweeps of this thread's chunk ----
@@ -572,7 +570,8 @@ __global__ void __launch_bounds__(H * X / 32, 3)
             yp[i] = __fadd2_rn(yp[i], h);
           }
         }
-        __syncthreads();   // every raw read of this tile is done
+        __syncthreads();   // every raw read of this tile (and of the previous look-ahead) is done
+        la_land(oLA, PL, jl, 1);                        // reduced at the end of this step
         // halo: previous tile's last HF filtered columns (zero before the first tile)
         for (int e = tid; e < 2 * H; e += NT) {
           const int r = e >> 1, qd = e & 1;
