@@ -67,6 +67,9 @@ struct SweepGeom {
   int P;      // pass-B L2 prefetch distance in items (env FBP_PREFETCH)
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
+  int dbg;    // developer timing mask, env FBP_DBG (results invalid when nonzero): pass B bit 0
+              // skips the FHT steps, bit 1 the epilogue, bit 2 the fills; sweep bit 3
+              // skips every TMA load
 };
 
 // Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at

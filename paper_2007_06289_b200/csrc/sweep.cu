@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     //   look-ahead: box of H rows x PL columns from column jt*X
     const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
     auto tma_issue = [&](const CUtensorMap* mp, int ob, int col, unsigned bytes, int bi) {
-      if (tid == 0) {
+      if (tid == 0 && !(g.dbg & 8)) {
         fence_proxy_async();
         const unsigned bar = smem_u32(oBar + 2 * bi);
         mbar_expect_tx(bar, bytes);
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       }
     };
     auto tma_wait = [&](int bi) {
-      mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
+      if (!(g.dbg & 8)) mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
       ph ^= 1u << bi;
     };
     auto land = [&](int jt) { tma_issue(&tmapF, oF, jt * X - 8, H * PF * 4, 0); };
@@ -681,6 +681,30 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 // For PAIR 1 the image rows are staged into shared memory by cp.async while
 // the FHT steps run.  Two CTAs per SM; no cross-item prefetch.
 // ===========================================================================
+// Pass-B item position (slice, channel, x tile).  Items are visited with the grid
+// stride; the stride is decomposed once and added with mixed-radix carries, so the
+// loop needs no 64-bit division.
+struct PbPos {
+  int sl, ch, xi;
+};
+__device__ __forceinline__ PbPos pb_pos(long long t, int nx, int H) {
+  const long long per = (long long)nx * H;
+  PbPos p;
+  p.sl = (int)(t / per);
+  const int rem = (int)(t - (long long)p.sl * per);
+  p.ch = rem / nx;
+  p.xi = rem - p.ch * nx;
+  return p;
+}
+__device__ __forceinline__ PbPos pb_add(PbPos a, const PbPos& d, int nx, int H) {
+  a.xi += d.xi;
+  if (a.xi >= nx) { a.xi -= nx; ++a.ch; }
+  a.ch += d.ch;
+  if (a.ch >= H) { a.ch -= H; ++a.sl; }
+  a.sl += d.sl;
+  return a;
+}
+
 template <int R1, int R2, int XB, int PAIR, bool DB>
 __global__ void __launch_bounds__(256, 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
@@ -723,28 +747,24 @@ __global__ void __launch_bounds__(256, 2)
   // of channel ch (3D box PI x NB x 1, columns j' = xs - HI + NB.., zero-filled
   // outside the row), for pair 1 the XB image rows x0.. (2D box NB x XB); plus an
   // L2 prefetch of the boxes of item tt + P*gridDim.x
-  auto issue = [&](long long tt, int bb) {
-    if (tid != 0 || tt >= nitems) return;
-    const long long per2 = (long long)nx * H;
+  const int nsl = (int)(nitems / ((long long)nx * H));
+  const PbPos step = pb_pos(gridDim.x, nx, H);
+  const PbPos stepP = pb_pos((long long)g.P * gridDim.x, nx, H);
+  auto issue = [&](const PbPos& pt, int bb) {
+    if (tid != 0 || pt.sl >= nsl || (g.dbg & 4)) return;
     if (g.P > 0) {
-      const long long tp = tt + (long long)g.P * gridDim.x;
-      if (tp < nitems) {
-        const long long slp = tp / per2;
-        const int remp = (int)(tp - slp * per2);
-        const int chp = remp / nx;
-        const int x0p = (remp - chp * nx) * XB;
+      const PbPos pp = pb_add(pt, stepP, nx, H);
+      if (pp.sl < nsl) {
+        const int x0p = pp.xi * XB;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int xs = (q == 0) ? x0p : (N - x0p - XB);
-          tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (int)((slp * 4 + 2 * PAIR + q) * H + chp));
+          tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (pp.sl * 4 + 2 * PAIR + q) * H + pp.ch);
         }
-        if (PAIR == 1) tma_prefetch_2d(&tmapI, chp * NB, (int)(slp * N + x0p));
+        if (PAIR == 1) tma_prefetch_2d(&tmapI, pp.ch * NB, pp.sl * N + x0p);
       }
     }
-    const long long sl2 = tt / per2;
-    const int rem2 = (int)(tt - sl2 * per2);
-    const int ch2 = rem2 / nx;
-    const int x02 = (rem2 - ch2 * nx) * XB;
+    const int sl2 = pt.sl, ch2 = pt.ch, x02 = pt.xi * XB;
     fence_proxy_async();
     const unsigned bar = smem_u32(oBar + 2 * bb);
     mbar_expect_tx(bar, 2u * NB * PI * 4 + (PAIR == 1 ? (unsigned)XB * PG * 4 : 0u));
@@ -752,29 +772,26 @@ __global__ void __launch_bounds__(256, 2)
     for (int q = 0; q < 2; ++q) {
       const int xs = (q == 0) ? x02 : (N - x02 - XB);
       tma_load_3d(smem_u32(oIn0 + bb * IN_SZ + q * NB * PI), &tmapR, xs - HI + NB, 0,
-                  (int)((sl2 * 4 + 2 * PAIR + q) * H + ch2), bar);
+                  (sl2 * 4 + 2 * PAIR + q) * H + ch2, bar);
     }
-    if (PAIR == 1) tma_load_2d(smem_u32(oG0 + bb * G_SZ), &tmapI, ch2 * NB, (int)(sl2 * N + x02), bar);
+    if (PAIR == 1) tma_load_2d(smem_u32(oG0 + bb * G_SZ), &tmapI, ch2 * NB, sl2 * N + x02, bar);
   };
-  issue(blockIdx.x, 0);
+  PbPos cur = pb_pos(blockIdx.x, nx, H);
+  issue(cur, 0);
   int bb = 0;
 
-  for (long long t = blockIdx.x; t < nitems; t += gridDim.x) {
-    const long long per = (long long)nx * H;
-    const long long sl = t / per;
-    const int rem = (int)(t - sl * per);
-    const int ch = rem / nx;
-    const int x0 = (rem - ch * nx) * XB;
-    float* out = img + sl * (long long)N * N;
+  for (; cur.sl < nsl; cur = pb_add(cur, step, nx, H)) {
+    const int ch = cur.ch;
+    const int x0 = cur.xi * XB;
     const int oIn = oIn0 + bb * IN_SZ, oG = oG0 + bb * G_SZ;
-    if (DB) issue(t + gridDim.x, bb ^ 1);               // buffer freed by the previous item
+    if (DB) issue(pb_add(cur, step, nx, H), bb ^ 1);   // buffer freed by the previous item
     // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
     //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
     //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
-    mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);
+    if (!(g.dbg & 4)) mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);   // bit 2: do not wait (timing only)
     ph ^= 1u << bb;
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
-    {
+    if (!(g.dbg & 1)) {
       constexpr int nch = (HS + XB) / C1;
       constexpr int per_fam = (NB / NR1) * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
@@ -794,7 +811,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
     // ---- step 2: both families, core columns -> park (aliasing the input) ----
-    {
+    if (!(g.dbg & 1)) {
       constexpr int nch = XB / C2;
       constexpr int per_fam = NR1 * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
@@ -821,37 +838,38 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
     // ---- epilogue ----
-    if (PAIR == 0) {
+    if (g.dbg & 2) {
+    } else if (PAIR == 0) {
       constexpr int nq = XB / 4;
+      float* const outc = img + ((long long)cur.sl * N + ch * NB) * N + x0;   // image rows ch*NB..
       for (int e = tid; e < NB * nq; e += NT) {
         const int rf = e / nq, kq = e - rf * nq;
         const float4 a = ld4(oIn + rf * PK + 4 * kq);
         const float4 m = ld4(oIn + (NB + rf) * PK + XB - 4 - 4 * kq);
-        const int x = x0 + 4 * kq;
-        if (x < N) {
+        if (x0 + 4 * kq < N) {
           const float4 o = make_float4(scale * (a.x + m.w), scale * (a.y + m.z), scale * (a.z + m.y),
                                        scale * (a.w + m.x));
-          *reinterpret_cast<float4*>(out + (long long)(ch * NB + rf) * N + x) = o;
+          *reinterpret_cast<float4*>(outc + rf * N + 4 * kq) = o;
         }
       }
     } else {
       // lanes: 8 row-quads of one image row x 4 image rows per warp (coalesced 128 B rows)
       constexpr int gq = NB / 4;
+      float* const outc = img + ((long long)cur.sl * N + x0) * N + ch * NB;   // image rows x0..
       for (int e = tid; e < XB * gq; e += NT) {
         const int i = e / gq, rq = e - i * gq;
-        const int x = x0 + i;
-        if (x >= N) continue;
+        if (x0 + i >= N) continue;
         const int rf = 4 * rq;
         float4 o = ld4(oG + i * PG + rf);
         o.x += scale * (sm[oIn + rf * PK + i] + sm[oIn + (NB + rf) * PK + XB - 1 - i]);
         o.y += scale * (sm[oIn + (rf + 1) * PK + i] + sm[oIn + (NB + rf + 1) * PK + XB - 1 - i]);
         o.z += scale * (sm[oIn + (rf + 2) * PK + i] + sm[oIn + (NB + rf + 2) * PK + XB - 1 - i]);
         o.w += scale * (sm[oIn + (rf + 3) * PK + i] + sm[oIn + (NB + rf + 3) * PK + XB - 1 - i]);
-        *reinterpret_cast<float4*>(out + (long long)x * N + ch * NB + rf) = o;
+        *reinterpret_cast<float4*>(outc + i * N + rf) = o;
       }
     }
     __syncthreads();                                   // park / staging reused by the next item
-    if (!DB) issue(t + gridDim.x, 0);
+    if (!DB) issue(pb_add(cur, step, nx, H), 0);
     if (DB) bb ^= 1;
   }
 }

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Top shared-memory instructions by excessive (bank-conflict) wavefronts (no GPU).
 
-  python tools/ncu_smem_conflicts.py report.ncu-rep k_sweep_ws [top]
+  [NCU_INST=substring] python tools/ncu_smem_conflicts.py report.ncu-rep k_sweep_ws [top]
 """
 import csv
 import io
@@ -13,6 +13,16 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}",
                       "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
+# several kernels (template instances) may match: keep the one whose full name
+# contains $NCU_INST (default: the first)
+inst = __import__("os").environ.get("NCU_INST", "")
+blocks = []
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        blocks.append([r])
+    elif blocks:
+        blocks[-1].append(r)
+rows = next(b for b in blocks if inst in b[0][1])
 h = rows[1]
 iS, iX, iW, iA = (h.index("Source"), h.index("L1 Wavefronts Shared Excessive"),
                   h.index("L1 Wavefronts Shared"), h.index("Address"))
