@@ -298,6 +298,39 @@ __device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], flo
 //   S1     : H x PS  step-1 output, core [HS, HS+X), halo [0, HS)
 //   ring   : (D+1) x H x 4  anticausal tile aggregates
 // ===========================================================================
+// S1 halo copy plan of the sweep: row (b', c) of step 2 reads S1 virtual columns
+// >= HS - O2 - c*b' only, so at the end of a tile only the quads
+// qd < (O2 + (c*b' & ~3))/4 + 1 of each row (cols HS - 4 qd ..) move to the halo.
+// The needed (row, quad) pairs in row-major order are dealt round-robin to the NT
+// threads; v[kk*NT + t] = S1 offset of thread t's kk-th quad, 0xffff for none.
+template <int H, int HS, int O2, int PS, int NT>
+struct HaloTab {
+  static constexpr int MAXQ = (HS + 4) / 4;
+  static constexpr int count() {
+    int n = 0;
+    for (int rr = 0; rr < H; ++rr) {
+      const int cb = (rr & 7) * (rr >> 3);
+      const int nq = (O2 + (cb & ~3)) / 4 + 1;
+      n += nq < MAXQ ? nq : MAXQ;
+    }
+    return n;
+  }
+  static constexpr int NKH = (count() + NT - 1) / NT;
+  unsigned short v[NKH * NT];
+  constexpr HaloTab() : v() {
+    for (int i = 0; i < NKH * NT; ++i) v[i] = 0xffff;
+    int n = 0;
+    for (int rr = 0; rr < H; ++rr) {
+      const int cb = (rr & 7) * (rr >> 3);
+      int nq = (O2 + (cb & ~3)) / 4 + 1;
+      if (nq > MAXQ) nq = MAXQ;
+      for (int qd = 0; qd < nq; ++qd, ++n) v[n] = (unsigned short)(rr * PS + HS - 4 * qd);
+    }
+  }
+};
+template <int H, int HS, int O2, int PS, int NT>
+__device__ constexpr HaloTab<H, HS, O2, PS, NT> kHaloTab{};
+
 template <int H, int X, bool IIR, bool BETA>
 __global__ void __launch_bounds__(H * X / 32, 3)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
@@ -321,6 +354,10 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 
   const int tid = threadIdx.x;
   const int D = g.D;
+  using HT = HaloTab<H, HS, O2, PS, NT>;
+  unsigned hoff[HT::NKH];                                // this thread's S1 halo quads
+#pragma unroll
+  for (int kk = 0; kk < HT::NKH; ++kk) hoff[kk] = kHaloTab<H, HS, O2, PS, NT>.v[kk * NT + tid];
   // 3 mbarriers (F tile, look-ahead slot, prologue temp in S1), then the work item
   const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
   int* s_item = reinterpret_cast<int*>(sm + oBar + 6);
@@ -653,17 +690,16 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       slot_j = (slot_j == D) ? 0 : slot_j + 1;
       // ---- S1 halo for the next tile: row (b', c) of step 2 reads virtual columns
       //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
+      // the needed (row, quad) pairs, dealt round-robin to the threads (HaloTab):
+      // at most NKH live quads per thread, all loads issued before the stores
       if (j >= j0) {
-        constexpr int MAXQ = (HS + 4) / 4;
-        const int r = tid >> 1;
-        for (int rr = r; rr < H; rr += NT / 2) {
-          const int cb = (rr & 7) * (rr >> 3);
-          const int nq = (O2 + (cb & ~3)) / 4 + 1;
-          for (int qd = tid & 1; qd < nq && qd < MAXQ; qd += 2) {
-            const int c0 = HS + 4 - 4 * (qd + 1);
-            st4(oS + rr * PS + c0, ld4(oS + rr * PS + X + c0));
-          }
-        }
+        float4 tq[HT::NKH];
+#pragma unroll
+        for (int kk = 0; kk < HT::NKH; ++kk)
+          if (hoff[kk] != 0xffffu) tq[kk] = ld4(oS + (int)hoff[kk] + X);
+#pragma unroll
+        for (int kk = 0; kk < HT::NKH; ++kk)
+          if (hoff[kk] != 0xffffu) st4(oS + (int)hoff[kk], tq[kk]);
       }
     }
   }
