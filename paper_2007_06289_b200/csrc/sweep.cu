@@ -684,10 +684,12 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           }
         }
       }
+      // look-ahead reduction before the barrier: it needs only the landing (every
+      // thread waits on the mbarrier) and writes ring entries its own warp reads
       if (IIR && jl < nt) tma_wait(1);
-      __syncthreads();
       if (IIR) la_finish(oLA, PL, jl, slot_j);          // tile j + D + 1 reuses tile j's slot
       slot_j = (slot_j == D) ? 0 : slot_j + 1;
+      __syncthreads();                                   // step 2's S1 reads precede the halo copy
       // ---- S1 halo for the next tile: row (b', c) of step 2 reads virtual columns
       //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
       // the needed (row, quad) pairs, dealt round-robin to the threads (HaloTab):
