@@ -258,6 +258,37 @@ def run_fbp(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_clean, ms = float(t[0]), float(t[1])
 
+    # ---- NEXT-1: forward FHT (fbp_fht_forward, Eq.17) of this step's images ----
+    fwd = None
+    if not args.no_forward:
+        lin_f = torch.empty_like(S)
+        for _ in range(3):
+            plan.forward(img, out=lin_f, stream=stream)
+        kf = max(1, min(args.steps, 20))
+        torch.cuda.synchronize(dev)
+        barrier()
+        plan.profile(True)
+        e0.record(stream)
+        for _ in range(kf):
+            plan.forward(img, out=lin_f, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms_f = e0.elapsed_time(e1)
+        kt_f = plan.kernel_times()
+        plan.profile(False)
+        tf = torch.tensor([ms_f], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+        ms_f = float(tf[0])
+        alg_f = 36.0 * N * N                   # image read (4 N^2 B) + linogram write (32 N^2 B)
+        fwd = {"value": world * B * kf / (ms_f / 1e3), "unit": UNIT, "steps": kf, "ms_per_step": ms_f / kf,
+               "input": "this step's reconstructed images", "gpu_launches_per_step": plan.launch_count(),
+               "kernel_ms_per_step": {k: v[0] / kf for k, v in kt_f.items() if v[1] > 0},
+               "roofline": {"bound": "hbm", "alg_bytes_per_slice": alg_f, "unit": "GB/s per GPU",
+                            "achieved": alg_f * B * kf / (ms_f / 1e3) / 1e9}}
+        del lin_f
+
     # ---- end to end through the public host-buffer C-ABI call ----
     e2e = None
     if not args.no_e2e:
@@ -323,6 +354,10 @@ def run_fbp(args):
             "clocks": clocks,
             "e2e": e2e,
         }
+        if fwd is not None:
+            fwd["roofline"]["peak"] = peak
+            fwd["roofline"]["frac"] = fwd["roofline"]["achieved"] / peak
+            line["next"] = {"fht_forward": fwd}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(N, b, a)
         print(json.dumps(line), flush=True)
@@ -343,6 +378,7 @@ def main():
     ap.add_argument("--e2e-batch", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-forward", action="store_true", help="skip the NEXT-1 forward-FHT line item")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

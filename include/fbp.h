@@ -96,6 +96,21 @@ FBP_API fbp_status fbp_fht_backproject(const fbp_plan* plan, const float* lin, f
                                float scale, void* cuda_stream);
 
 /*
+ * fbp_fht_forward -- forward dyadic projection (discrete Radon transform along
+ * dyadic patterns) by the Fast Hough Transform, the four families of Eq.16:
+ *   lin[f][t][s] = sum_{y<N} G_f[y][s - N + d_t(y)]     PAPER.md:199-202 (Eq.17),
+ *   G_0 = image[y][x], G_1 = image[y][N-1-x], G_2 = image[x][y], G_3 = image[N-1-x][y]
+ *   (Eq.16, reading R4); terms with a column outside [0, N) are dropped.
+ *   image: device [batch][N][N];  lin: device [batch][4][N][2N] (overwritten).
+ *   Additions only (bit-exact on integer-valued input); the exact adjoint of
+ *   fbp_fht_backproject's per-family sums.  Uses the plan's workspace, so calls on
+ *   one plan must not run concurrently.  Errors: FBP_ERR_PARAM (NULL / misaligned
+ *   pointer, batch outside [0, max_batch]), FBP_ERR_CUDA.
+ */
+FBP_API fbp_status fbp_fht_forward(const fbp_plan* plan, const float* image, float* lin, int batch,
+                                   void* cuda_stream);
+
+/*
  * fbp_reconstruct -- the whole hot path: IIR ramp filter then FHT back
  * projection with weight w = 1/N (reading R7).
  *   sino: device [batch][4][N][2N];  image: device [batch][N][N].
@@ -131,9 +146,10 @@ FBP_API long long fbp_plan_launch_count(const fbp_plan* plan);
  * Per-kernel device timing (CUDA events recorded on the launching stream around
  * every kernel while enabled).  fbp_plan_profile(plan, 1) clears and enables,
  * 0 disables.  fbp_plan_kernel_times synchronises on the recorded events and
- * writes, for kind k in {0: IIR, 1: FHT pass A, 2: FHT pass B}, the summed
- * milliseconds ms[k] and launch count launches[k] (arrays of length `kinds`,
- * at most 3) since the last enable, then clears the record.
+ * writes, for kind k in {0: IIR, 1: FHT pass A, 2: FHT pass B, 3: forward FHT
+ * pass A, 4: forward FHT pass B}, the summed milliseconds ms[k] and launch count
+ * launches[k] (arrays of length `kinds`, at most 5) since the last enable, then
+ * clears the record.
  */
 FBP_API fbp_status fbp_plan_profile(fbp_plan* plan, int enable);
 FBP_API fbp_status fbp_plan_kernel_times(fbp_plan* plan, double* ms, long long* launches, int kinds);

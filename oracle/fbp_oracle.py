@@ -257,6 +257,30 @@ def forward_project(img: np.ndarray) -> np.ndarray:
     return S
 
 
+def forward_sample(img: np.ndarray, f: int, t: int, s: int) -> float:
+    """One linogram sample of the forward projection, direct definition (Eq.17).
+
+    PAPER.md:199-202 (Eq.17) discretised along dyadic patterns (R1-R3), family
+    view G_f of Eq.16 (R4): S[f][t][s] = sum_{y<N} G_f[y][s - N + d_t(y)], terms
+    outside [0, N) dropped, summed in order y = 0..N-1; d_t(y) by the closed form
+    of R3 for all y at once.  Same definition as ``forward_project`` (pinned against
+    it in tests/test_oracle_pins.py), one sample at a time for full-size checks.
+    """
+    G = family_views(np.asarray(img, dtype=np.float64))[f]
+    N = G.shape[0]
+    n = N.bit_length() - 1
+    y = np.arange(N, dtype=np.int64)
+    d = np.zeros(N, dtype=np.int64)
+    for k in range(n):
+        d += ((y >> (n - 1 - k)) & 1) * (((t >> k) + 1) // 2)
+    x = s - N + d
+    ok = (x >= 0) & (x < N)
+    acc = 0.0
+    for yy in y[ok]:
+        acc += float(G[yy, x[yy]])
+    return acc
+
+
 def dyadic_offsets_column(N: int, y: int) -> np.ndarray:
     """d_t(y) for all t at one row y, by the closed form of R3 (vectorised over t)."""
     n = N.bit_length() - 1

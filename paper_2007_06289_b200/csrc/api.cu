@@ -413,7 +413,8 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   // ---- workspace, sized for a group of slices ----
   const Geometry& g = p->g;
   const size_t f_slice = p->fast ? 0 : (size_t)4 * g.N * g.W * sizeof(float);
-  const size_t r_slice = (size_t)4 * g.NB * g.H * g.WR * sizeof(float);
+  // R also serves fbp_fht_forward's pass-A output (fwd_workspace_floats per slice)
+  const size_t r_slice = std::max((size_t)4 * g.NB * g.H * g.WR, fwd_workspace_floats(g)) * sizeof(float);
   // fast path: the whole max_batch in one group up to 8 GiB of R (a small trailing
   // group would leave most of the 444 sweep CTA slots idle); general path: 256 MiB
   const size_t budget = p->fast ? ((size_t)8 << 30) : ((size_t)256 << 20);
@@ -508,6 +509,30 @@ fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image
     if (e != cudaSuccess) {
       p->launches = launches;
       return cuda_fail(e, "fbp_fht_backproject");
+    }
+  }
+  p->launches = launches;
+  return FBP_OK;
+}
+
+fbp_status fbp_fht_forward(const fbp_plan* p, const float* image, float* lin, int batch, void* stream) {
+  fbp_status s = check_call(p, image, lin, batch);
+  if (s != FBP_OK || batch == 0) return s;
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  const long long lin_elems = 4LL * p->g.N * p->g.W;
+  const long long img_elems = (long long)p->g.N * p->g.N;
+  const size_t per = fwd_workspace_floats(p->g) * sizeof(float);
+  const int grp = (int)std::max<size_t>(1, std::min<size_t>(p->R_bytes / per, 16383));
+  const cudaStream_t st = (cudaStream_t)stream;
+  for (int s0 = 0; s0 < batch; s0 += grp) {
+    const int ns = std::min(grp, batch - s0);
+    cudaError_t e = timed(p, 3, st, [&] { return launch_fwd_a(image + s0 * img_elems, p->R, ns, p->g, st, &launches); });
+    if (e == cudaSuccess)
+      e = timed(p, 4, st, [&] { return launch_fwd_b(p->R, lin + s0 * lin_elems, ns, p->g, st, &launches); });
+    if (e != cudaSuccess) {
+      p->launches = launches;
+      return cuda_fail(e, "fbp_fht_forward");
     }
   }
   p->launches = launches;
@@ -650,7 +675,7 @@ fbp_status fbp_plan_profile(fbp_plan* p, int enable) {
 }
 
 fbp_status fbp_plan_kernel_times(fbp_plan* p, double* ms, long long* launches, int kinds) {
-  if (!p || kinds < 0 || kinds > 3 || (kinds > 0 && (!ms || !launches)))
+  if (!p || kinds < 0 || kinds > 5 || (kinds > 0 && (!ms || !launches)))
     return fail(FBP_ERR_PARAM, "fbp_plan_kernel_times: bad arguments");
   DeviceGuard guard(p->device);
   for (int k = 0; k < kinds; ++k) {

@@ -99,4 +99,12 @@ cudaError_t launch_fht_pass_a(const float* lin, float* R, int slices, int f0, in
 cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, float scale,
                               const Geometry& g, cudaStream_t st, int* launches);
 
+// Forward FHT (fwd.cu, Eq.17): image [slices][N][N] -> R_A (workspace of
+// fwd_workspace_floats per slice) -> linogram [slices][4][N][2N].  slices <= 16383.
+size_t fwd_workspace_floats(const Geometry& g);
+cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry& g, cudaStream_t st,
+                         int* launches);
+cudaError_t launch_fwd_b(const float* RA, float* lin, int slices, const Geometry& g, cudaStream_t st,
+                         int* launches);
+
 }  // namespace fbp

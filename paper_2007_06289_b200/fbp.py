@@ -8,6 +8,7 @@ missing or the device is not an sm_100 B200 it raises.
     img  = plan.reconstruct(sino)            # sino: float32 cuda [B, 4, N, 2N]
     F    = plan.iir_filter(sino)             # Eq.12-13
     bp   = plan.backproject(F, scale=1/N)    # Eq.19-22
+    lin  = plan.forward(img)                 # Eq.17 (forward FHT)
 """
 from __future__ import annotations
 
@@ -24,11 +25,11 @@ FBP_STATUS = {0: "FBP_OK", 1: "FBP_ERR_PLAN", 2: "FBP_ERR_PARAM", 3: "FBP_ERR_UN
               4: "FBP_ERR_CUDA", 5: "FBP_ERR_NOMEM", 6: "FBP_ERR_DEVICE"}
 
 EXPORTED = ["fbp_plan_create", "fbp_plan_destroy", "fbp_iir_filter", "fbp_fht_backproject",
-            "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
+            "fbp_fht_forward", "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
             "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_path", "fbp_plan_profile",
             "fbp_plan_kernel_times"]
 
-KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b")
+KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b", "fwd_pass_a", "fwd_pass_b")
 
 
 class FbpError(RuntimeError):
@@ -54,6 +55,8 @@ def lib():
     L.fbp_iir_filter.restype = i
     L.fbp_fht_backproject.argtypes = [vp, vp, vp, i, f, vp]
     L.fbp_fht_backproject.restype = i
+    L.fbp_fht_forward.argtypes = [vp, vp, vp, i, vp]
+    L.fbp_fht_forward.restype = i
     L.fbp_reconstruct.argtypes = [vp, vp, vp, i, vp]
     L.fbp_reconstruct.restype = i
     L.fbp_reconstruct_host.argtypes = [vp, vp, vp, i]
@@ -139,9 +142,10 @@ class Plan:
 
     def kernel_times(self) -> dict:
         """{kind: (total_ms, launches)} since the last profile(True); clears the record."""
-        ms = (ctypes.c_double * 3)()
-        n = (ctypes.c_longlong * 3)()
-        _check(lib().fbp_plan_kernel_times(self._h, ms, n, 3))
+        k = len(KERNEL_KINDS)
+        ms = (ctypes.c_double * k)()
+        n = (ctypes.c_longlong * k)()
+        _check(lib().fbp_plan_kernel_times(self._h, ms, n, k))
         return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_KINDS)}
 
     # ------------------------------------------------------------- checks
@@ -179,6 +183,23 @@ class Plan:
         out = self._img_out(out, x.shape[0])
         _check(lib().fbp_fht_backproject(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
                                          float(scale), _stream_ptr(stream)))
+        return out
+
+    def forward(self, image: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """Forward dyadic projection (Eq.17), image [B, N, N] -> linogram [B, 4, N, 2N]."""
+        N = self.n
+        if not (isinstance(image, torch.Tensor) and image.is_cuda and image.dtype == torch.float32):
+            raise TypeError("image must be a float32 CUDA tensor")
+        if image.dim() == 2:
+            image = image.unsqueeze(0)
+        if tuple(image.shape[1:]) != (N, N) or not image.is_contiguous():
+            raise ValueError(f"image must be a contiguous [B, {N}, {N}] tensor, got {tuple(image.shape)}")
+        B = image.shape[0]
+        if out is None:
+            out = torch.empty((B, 4, N, 2 * N), device=image.device, dtype=torch.float32)
+        else:
+            out = self._lin(out, "out")
+        _check(lib().fbp_fht_forward(self._h, image.data_ptr(), out.data_ptr(), B, _stream_ptr(stream)))
         return out
 
     def reconstruct(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):

@@ -173,3 +173,20 @@ def integer_linogram(N: int, batch: int, seed: int, lo: int = -511, hi: int = 51
     g.manual_seed(int(seed))
     x = torch.randint(lo, hi + 1, (batch, 4, N, 2 * N), generator=g, dtype=torch.int64)
     return x.to(torch.float32).to(device)
+
+
+def integer_image(N: int, batch: int, seed: int, lo: int = -511, hi: int = 511,
+                  device="cpu") -> torch.Tensor:
+    """Integer-valued [batch][N][N] float32 image in [lo, hi] (bit-exact forward FHT tests)."""
+    g = torch.Generator(device="cpu")
+    g.manual_seed(int(seed))
+    x = torch.randint(lo, hi + 1, (batch, N, N), generator=g, dtype=torch.int64)
+    return x.to(torch.float32).to(device)
+
+
+def random_image(N: int, batch: int, seed: int, device="cpu") -> torch.Tensor:
+    """Uniform random [batch][N][N] float32 image in [0, 1) (forward FHT stress)."""
+    g = torch.Generator(device="cpu")
+    g.manual_seed(int(seed))
+    x = torch.rand((batch, N, N), generator=g, dtype=torch.float64)
+    return x.to(torch.float32).to(device)

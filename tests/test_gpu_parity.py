@@ -287,3 +287,78 @@ def test_fast_path_determinism_host_and_composition(fbp):
     F = plan.iir_filter(S.cuda())
     bp = plan.backproject(F, scale=1.0 / N).cpu()
     assert rel_err(bp.numpy(), d1.numpy()) < 1e-5
+
+
+# ----------------------------------------------------------- forward FHT (NEXT-1)
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 32, 64, 128, 256, 512])
+def test_forward_integer_bit_exact(fbp, N):
+    """fbp_fht_forward == oracle fht_forward (Eq.17) exactly on integer images."""
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=3)
+    img = P.integer_image(N, 3, seed=7 * N)
+    out = plan.forward(img.cuda()).cpu().numpy()
+    for i in range(3):
+        ref = O.fht_forward(img[i].numpy().astype(np.float64))
+        assert np.array_equal(out[i].astype(np.float64), ref), (N, i)
+
+
+@pytest.mark.parametrize("N", [64, 1024])
+def test_forward_float_within_tolerance(fbp, N):
+    """Random float images: fp32 sums vs fp64 oracle within the 1e-4 gate (samples at
+    N=1024, every sample at N=64)."""
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    img = P.random_image(N, 2, seed=N + 5)
+    out = plan.forward(img.cuda()).cpu().numpy()
+    im1 = img[1].numpy().astype(np.float64)
+    if N <= 64:
+        ref = O.fht_forward(im1)
+        assert rel_err(out[1], ref) <= TOL
+    else:
+        rng = np.random.default_rng(N)
+        peak = float(im1.sum(axis=0).max())       # t = 0 row of family 0: column sums
+        for _ in range(24):
+            f, t, s_ = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+            ref = O.forward_sample(im1, f, t, s_)
+            assert abs(float(out[1, f, t, s_]) - ref) <= TOL * peak, (f, t, s_)
+
+
+def test_forward_full_size_sampled_and_adjoint(fbp):
+    """N=2048 (config 3 size): integer image, sampled outputs exact vs the direct
+    definition; adjoint identity <fwd(img), P> = <img, BP_families(P)> exactly."""
+    N = 2048
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    img = P.integer_image(N, 1, seed=2048, lo=-7, hi=7)
+    S = plan.forward(img.cuda()).cpu().numpy()[0].astype(np.float64)
+    im = img[0].numpy().astype(np.float64)
+    rng = np.random.default_rng(3)
+    for _ in range(12):
+        f, t, s_ = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+        assert S[f, t, s_] == O.forward_sample(im, f, t, s_), (f, t, s_)
+    # every (family, t) row sums to the image total (each pixel lies on one line)
+    assert np.all(S.sum(axis=2) == im.sum())
+    # adjoint: family-summed BP with weight 1 of an integer linogram
+    Pl = P.integer_linogram(N, 1, seed=11, lo=-3, hi=3)
+    bp = plan.backproject(Pl.cuda(), scale=1.0).cpu().numpy()[0].astype(np.float64)
+    lhs = float(np.sum(S * Pl[0].numpy().astype(np.float64)))
+    rhs = float(np.sum(im * bp))
+    assert lhs == rhs
+
+
+def test_forward_edge_cases(fbp):
+    N = 64
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    assert plan.forward(torch.zeros((0, N, N), device="cuda")).shape == (0, 4, N, 2 * N)
+    with pytest.raises(ValueError):
+        plan.forward(torch.zeros((1, N, N + 1), device="cuda"))
+    with pytest.raises(ValueError):
+        plan.forward(torch.zeros((1, N, 2 * N), device="cuda")[:, :, ::2])
+    with pytest.raises(fbp.FbpError):
+        plan.forward(torch.zeros((3, N, N), device="cuda"))       # batch > max_batch
+    # a single unit pixel lights exactly one sample per (family, t) row
+    img = torch.zeros((1, N, N), device="cuda")
+    img[0, 5, 9] = 1.0
+    S = plan.forward(img).cpu().numpy()[0]
+    assert np.all(S.sum(axis=2) == 1.0) and np.all((S == 1.0).sum(axis=2) == 1)

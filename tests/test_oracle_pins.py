@@ -184,6 +184,19 @@ def test_forward_2x2_spec_example():
     assert np.array_equal(S, np.array(g2["S"], dtype=float))
 
 
+@pytest.mark.parametrize("N", [2, 8, 32])
+def test_forward_sample_matches_forward_project(N):
+    """forward_sample (one sample, closed-form d_t) == forward_project (recursive
+    pattern table, pinned below by brute force / SPEC identities) at every sample."""
+    rng = np.random.default_rng(100 + N)
+    img = rng.integers(-50, 50, size=(N, N)).astype(float)
+    S = O.forward_project(img)
+    for f in range(4):
+        for t in range(N):
+            for s in range(2 * N):
+                assert O.forward_sample(img, f, t, s) == S[f, t, s]
+
+
 @pytest.mark.parametrize("N", [2, 4, 8, 16])
 def test_forward_brute_force_and_fht_forward_bit_exact(N):
     """SPEC.md:363/474: FHT == brute-force dyadic sums on random integer images, exactly;
