@@ -117,7 +117,7 @@ FBP_API fbp_status fbp_fht_forward(const fbp_plan* plan, const float* image, flo
  * Not required to equal fbp_fht_backproject(fbp_iir_filter(.), 1/N) bitwise.
  * On the fused fast path (fbp_plan_path) the anticausal recursion's carry into
  * each tile of X samples sums the next D tiles only; D is the smallest tile
- * count whose dropped impulse-response tail is <= 1e-12 of its l1 norm
+ * count whose dropped impulse-response tail is <= 1e-9 of its l1 norm
  * (reading R22).  Otherwise the recursion is exact.
  */
 FBP_API fbp_status fbp_reconstruct(const fbp_plan* plan, const float* sino, float* image, int batch,

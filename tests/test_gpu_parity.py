@@ -234,7 +234,7 @@ def _tail_lookahead(b, a, X, Dmax=16):
         h[i] = v
     tail = np.cumsum(np.abs(h)[::-1])[::-1]
     for d in range(1, Dmax + 1):
-        if tail[max(0, d * X - 2)] <= 1e-12 * tail[0]:
+        if tail[max(0, d * X - 2)] <= 1e-9 * tail[0]:
             return d
     return 0
 
