@@ -82,7 +82,7 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
                           const SweepGeom& g, cudaStream_t st, int* launches);
 bool sweep_supported(int N);
 size_t sweep_a_smem(const SweepGeom& g);
-size_t pair_b_smem(const SweepGeom& g);
+size_t pair_b_smem(const SweepGeom& g, int pair);
 
 // Kernel launchers (kernels.cu).  All asynchronous on `st`; return the launch error.
 // lane_mats: device [32][8*8], lane_mats[j] = A^(L*j).

@@ -744,7 +744,7 @@ __device__ __forceinline__ PbPos pb_add(PbPos a, const PbPos& d, int nx, int H) 
 }
 
 template <int R1, int R2, int XB, int PAIR, bool DB>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
              long long nitems, const __grid_constant__ CUtensorMap tmapR,
              const __grid_constant__ CUtensorMap tmapI) {
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(256, 2)
   // DB: two input (and staging) buffers, the next item's TMA boxes land while this
   // item computes
   constexpr int NBUF = DB ? 2 : 1;
-  constexpr int IN_SZ = 2 * NB * PI, G_SZ = XB * PG;
+  constexpr int IN_SZ = 2 * NB * PI, G_SZ = PAIR == 1 ? XB * PG : 0;   // pair 0 stages no image
   constexpr int oIn0 = 0;                             // [NBUF][2 fam][NB][PI]; park aliases it
   constexpr int oS = NBUF * IN_SZ;                    // [2 fam][NB][PS]
   constexpr int oG0 = oS + 2 * NB * PS;               // [NBUF][XB][PG] image rows (pair 1)
@@ -925,7 +925,7 @@ size_t sweep_a_smem(const SweepGeom& g) {
           2) * sizeof(float);
 }
 
-size_t pair_b_smem(const SweepGeom& g) {
+size_t pair_b_smem(const SweepGeom& g, int pair) {
   const bool db = g.XB <= 64;
   const int NB = g.NB, XB = g.XB;
   int m = 0;
@@ -937,7 +937,7 @@ size_t pair_b_smem(const SweepGeom& g) {
   const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
   const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB;
   const size_t nbuf = db ? 2 : 1;
-  return (nbuf * 2 * NB * PI + (size_t)2 * NB * PS + nbuf * XB * PG + 4) * sizeof(float);
+  return (nbuf * 2 * NB * PI + (size_t)2 * NB * PS + (pair == 1 ? nbuf * XB * PG : 0) + 4) * sizeof(float);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
@@ -1024,7 +1024,7 @@ template <int R1, int R2, int XB, int PAIR>
 static cudaError_t launch_b_t(const float* R, float* img, int slices, float scale,
                               const SweepGeom& g, cudaStream_t st) {
   auto kern = k_pair_b<R1, R2, XB, PAIR, (XB <= 64)>;
-  const size_t smem = pair_b_smem(g);
+  const size_t smem = pair_b_smem(g, PAIR);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per = 0;
