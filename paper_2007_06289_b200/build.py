@@ -56,7 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for o in objs:
         os.remove(o)
     with open(os.path.join(PKG, "ptxas_report.txt"), "w") as fh:
-        fh.write("\n".join(logs))
+        # compile times vary run to run; keep the report deterministic
+        fh.write("\n".join("\n".join(l for l in lg.splitlines() if "Compile time" not in l) for lg in logs))
     with open(stamp, "w") as fh:
         fh.write(dg)
     if verbose:
