@@ -398,6 +398,82 @@ def fht_forward(img: np.ndarray) -> np.ndarray:
     return S
 
 
+# --------------------------------------------------------------------------
+# §4.2  (r, theta) -> (s, t) transition (NEXT-2)
+# --------------------------------------------------------------------------
+
+def linogram_line_rtheta(f: int, t: int, s: int, N: int):
+    """(r, theta, |D|) of linogram sample (f, t, s): Eq.14 for the line model of R2.
+
+    PAPER.md:172-178 (Eq.14) relates (s, t) to (r, theta); here the exact line of
+    reading R2 is used: view line X'(tau) = A + k tau, Y' = tau, A = s - N + 0.5 -
+    0.5 k, k = t/(N-1), mapped to image coordinates per family (R4):
+      f=0: P0 = (A, 0), D = (k, 1)        f=1: P0 = (N - A, 0), D = (-k, 1)
+      f=2: P0 = (0, A), D = (1, k)        f=3: P0 = (0, N - A), D = (1, -k).
+    Unit normal n = (D_y, -D_x)/|D|, flipped so that theta = atan2(n_y, n_x) lies
+    in [0, pi) (R23); r = (P0 - c).n, c = (N/2, N/2).
+    """
+    k = t / (N - 1)
+    A = s - N + 0.5 - 0.5 * k
+    P0, D = {0: ((A, 0.0), (k, 1.0)), 1: ((N - A, 0.0), (-k, 1.0)),
+             2: ((0.0, A), (1.0, k)), 3: ((0.0, N - A), (1.0, -k))}[f]
+    L = math.hypot(D[0], D[1])
+    nx, ny = D[1] / L, -D[0] / L
+    th = math.atan2(ny, nx)
+    if th < 0.0 or th >= math.pi:
+        nx, ny = -nx, -ny
+        th = math.atan2(ny, nx)
+    r = (P0[0] - N / 2.0) * nx + (P0[1] - N / 2.0) * ny
+    return r, th, L
+
+
+def sinogram_sample(p: np.ndarray, theta: float, r: float, dr: float) -> float:
+    """Linear interpolation of a scanner sinogram p[k][j] at (theta, r) (R23).
+
+    PAPER.md:178 ("transition ... using linear interpolation"): linear in the
+    angle index u = theta/(pi/P) between rows k0 = floor(u) and k0 + 1, linear in
+    the bin index w = r/dr + (R-1)/2 within a row, bins outside [0, R) read 0; the
+    row after k = P-1 is row 0 at -r (p(r, theta + pi) = p(-r, theta)).
+    """
+    P, R = p.shape
+
+    def row(k, rr):
+        w = rr / dr + 0.5 * (R - 1)
+        j0 = math.floor(w)
+        b = w - j0
+        v = 0.0
+        if 0 <= j0 < R:
+            v += (1.0 - b) * p[k, j0]
+        if 0 <= j0 + 1 < R:
+            v += b * p[k, j0 + 1]
+        return v
+
+    u = theta / (math.pi / P)
+    k0 = min(int(math.floor(u)), P - 1)
+    a = u - k0
+    v0 = row(k0, r)
+    v1 = row(k0 + 1, r) if k0 + 1 < P else row(0, -r)
+    return (1.0 - a) * v0 + a * v1
+
+
+def resample_sinogram(p: np.ndarray, N: int, dr: float = 1.0) -> np.ndarray:
+    """Sinogram -> linogram (NEXT-2), S[f][t][s].  PAPER.md:172-188 (Eq.14-15).
+
+    Each linogram sample is the sinogram linearly interpolated at the (r, theta) of
+    its line (Eq.14 for the R2 line model) divided by the stretch factor of Eq.15,
+    k_t = |D| = sqrt(1 + (t/(N-1))^2) for that line model (R23): the linogram
+    integrates along the row coordinate (dY', Eq.17), the scanner along arc length.
+    """
+    p = np.asarray(p, dtype=np.float64)
+    S = np.zeros((4, N, 2 * N))
+    for f in range(4):
+        for t in range(N):
+            for s in range(2 * N):
+                r, th, L = linogram_line_rtheta(f, t, s, N)
+                S[f, t, s] = sinogram_sample(p, th, r, dr) / L
+    return S
+
+
 def combine(B: np.ndarray, w: float) -> np.ndarray:
     """Sum of the four family images (Eq.22), weight w (R7).
 

@@ -190,3 +190,24 @@ def random_image(N: int, batch: int, seed: int, device="cpu") -> torch.Tensor:
     g.manual_seed(int(seed))
     x = torch.rand((batch, N, N), generator=g, dtype=torch.float64)
     return x.to(torch.float32).to(device)
+
+
+def sinogram_of_ellipses(E: EllipseSet, N: int, n_angles: int, n_bins: int, dr: float = 1.0,
+                         dtype=torch.float64) -> torch.Tensor:
+    """Scanner sinogram p[k][j] of the ellipse phantom (arc-length line integrals,
+    whole line, no square restriction), float64.  Geometry (reading R23):
+    theta_k = k*pi/n_angles is the angle of the line normal n = (cos, sin) in image
+    coordinates (x = column, y = row), r_j = (j - (n_bins-1)/2) * dr is the signed
+    distance of the line from the image centre (N/2, N/2).  Per ellipse (textbook
+    projection of an ellipse): p = 2 rho a b sqrt(max(0, m^2 - q^2)) / m^2 with
+    m^2 = a^2 cos^2(theta - phi) + b^2 sin^2(theta - phi), q = r - (e - c).n."""
+    th = torch.arange(n_angles, dtype=dtype) * (math.pi / n_angles)
+    r = (torch.arange(n_bins, dtype=dtype) - 0.5 * (n_bins - 1)) * dr
+    c, sn = torch.cos(th).view(-1, 1), torch.sin(th).view(-1, 1)
+    out = torch.zeros((n_angles, n_bins), dtype=dtype)
+    for i in range(len(E.cx)):
+        m2 = (E.a[i] * torch.cos(th - E.phi[i])) ** 2 + (E.b[i] * torch.sin(th - E.phi[i])) ** 2
+        m2 = m2.view(-1, 1)
+        q = r.view(1, -1) - ((E.cx[i] - N / 2.0) * c + (E.cy[i] - N / 2.0) * sn)
+        out = out + 2.0 * E.rho[i] * E.a[i] * E.b[i] * torch.sqrt(torch.clamp(m2 - q * q, min=0.0)) / m2
+    return out

@@ -331,3 +331,115 @@ def test_iir_fbp_dc0_recovers_phantom():
     scale, rel = _fit(rec, ph)
     assert abs(scale - 1.0) < 0.25, scale
     assert rel < 0.35, rel
+
+
+# ------------------------------------------------- NEXT-2: (r,theta) -> (s,t)
+def _family_line_np(f, A, k, N):
+    """P0, D of the phantom generator's line model (input-side code, not the oracle)."""
+    import torch
+    from phantoms.generator import _family_line
+    (px, py), (dx, dy) = _family_line(f, torch.tensor(float(A), dtype=torch.float64),
+                                      torch.tensor(float(k), dtype=torch.float64), N)
+    return (float(px), float(py)), (float(dx), float(dy))
+
+
+def test_linogram_line_rtheta_geometry():
+    """Every point of the R2 line (phantom generator's model) satisfies (p - c).n = r;
+    theta ranges are the paper's four classes: f1 = L_v- [0, pi/4],
+    f3 = L_h- [pi/4, pi/2], f2 = L_h+ [pi/2, 3pi/4], f0 = L_v+ [3pi/4, pi) (t = 0: 0)."""
+    import math
+    N = 16
+    rng = np.random.default_rng(5)
+    rngs = {1: (0, math.pi / 4), 3: (math.pi / 4, math.pi / 2), 2: (math.pi / 2, 3 * math.pi / 4),
+            0: (3 * math.pi / 4, math.pi)}
+    for _ in range(200):
+        f, t, s = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+        r, th, L = O.linogram_line_rtheta(f, t, s, N)
+        k = t / (N - 1)
+        P0, D = _family_line_np(f, s - N + 0.5 - 0.5 * k, k, N)
+        assert abs(L - math.hypot(*D)) < 1e-12 and 0.0 <= th < math.pi
+        for tau in (0.0, 3.7, float(N)):
+            px, py = P0[0] + tau * D[0], P0[1] + tau * D[1]
+            assert abs((px - N / 2) * math.cos(th) + (py - N / 2) * math.sin(th) - r) < 1e-9
+        lo, hi = rngs[f]
+        if not (f == 0 and t == 0):
+            assert lo - 1e-12 <= th <= hi + 1e-12, (f, t, th)
+    assert O.linogram_line_rtheta(0, 0, 5, N)[1] == 0.0          # vertical line, normal along x
+
+
+def test_sinogram_sample_wrap_and_bins():
+    """Linear interpolation in both indices; the row after P-1 is row 0 at -r; bins
+    outside the detector read 0 (R23)."""
+    import math
+    P_, R_ = 8, 9
+    p = np.zeros((P_, R_))
+    p[0, 2] = 1.0                                  # r = (2 - 4) * 1 = -2 at theta = 0
+    # theta half-way between rows 7 and 8 == row 0 at -r: r = +2 reads p[0][2] with weight 1/2
+    th = (P_ - 0.5) * math.pi / P_
+    assert abs(O.sinogram_sample(p, th, 2.0, 1.0) - 0.5) < 1e-12
+    assert abs(O.sinogram_sample(p, 0.0, -1.5, 1.0) - 0.5) < 1e-12   # half-way between bins 2, 3
+    assert O.sinogram_sample(p, 0.0, 100.0, 1.0) == 0.0
+
+
+def test_resample_zero_and_linear():
+    N = 8
+    rng = np.random.default_rng(2)
+    p1, p2 = rng.normal(size=(16, 15)), rng.normal(size=(16, 15))
+    assert not O.resample_sinogram(np.zeros((16, 15)), N).any()
+    lhs = O.resample_sinogram(2.0 * p1 - 3.0 * p2, N)
+    rhs = 2.0 * O.resample_sinogram(p1, N) - 3.0 * O.resample_sinogram(p2, N)
+    assert np.allclose(lhs, rhs, atol=1e-12)
+
+
+def _blob_case(N, n_angles, dr, seed=0):
+    """Gaussian blobs: analytic sinogram p = A sqrt(2 pi) s exp(-q^2 / 2 s^2) and the
+    analytic linogram along the phantom generator's lines, A sqrt(2 pi) s exp(-d^2/2s^2)/|D|
+    (blobs far inside the square)."""
+    import math
+    rng = np.random.default_rng(seed)
+    blobs = [(N / 2 + rng.uniform(-0.25, 0.25) * N, N / 2 + rng.uniform(-0.25, 0.25) * N,
+              rng.uniform(0.5, 1.5), rng.uniform(N / 16, N / 8)) for _ in range(4)]
+    nb = int(math.ceil(N * math.sqrt(2) / dr)) + 4
+    th = np.arange(n_angles) * math.pi / n_angles
+    r = (np.arange(nb) - 0.5 * (nb - 1)) * dr
+    sino = np.zeros((n_angles, nb))
+    for ex, ey, A, sg in blobs:
+        q = r[None, :] - ((ex - N / 2) * np.cos(th)[:, None] + (ey - N / 2) * np.sin(th)[:, None])
+        sino += A * math.sqrt(2 * math.pi) * sg * np.exp(-q * q / (2 * sg * sg))
+    ref = np.zeros((4, N, 2 * N))
+    for f in range(4):
+        for t in range(N):
+            k = t / (N - 1)
+            for s in range(2 * N):
+                P0, D = _family_line_np(f, s - N + 0.5 - 0.5 * k, k, N)
+                L = math.hypot(*D)
+                for ex, ey, A, sg in blobs:
+                    d = ((ex - P0[0]) * D[1] - (ey - P0[1]) * D[0]) / L
+                    ref[f, t, s] += A * math.sqrt(2 * math.pi) * sg * math.exp(-d * d / (2 * sg * sg)) / L
+    return sino, ref
+
+
+def test_resample_smooth_blobs_second_order():
+    """PAPER.md:178 linear interpolation + Eq.15 stretch: on smooth blobs the error
+    vs the analytic linogram is O(h^2) (x4 per halving of the sampling), which only
+    an exact (r, theta) geometry and the right k_t direction give."""
+    errs = []
+    for n_angles, dr in ((64, 1.0), (128, 0.5)):
+        sino, ref = _blob_case(32, n_angles, dr)
+        S = O.resample_sinogram(sino, 32, dr)
+        errs.append(np.abs(S - ref).max() / np.abs(ref).max())
+    assert errs[1] < 6e-3 and errs[0] / errs[1] > 3.0, errs
+
+
+def test_resample_ellipses_close_to_analytic_linogram():
+    """Sharp ellipses (inside the square): relative RMS error ~1 % at N = 64 (edges are
+    not smooth), below the 2 % SPEC-style interpolation tolerance."""
+    import phantoms as P
+    N = 64
+    E = P.draw_ellipses(N, 6, (N / 16, N / 5), seed=N)
+    E.cx = N / 2 + 0.5 * (E.cx - N / 2)
+    E.cy = N / 2 + 0.5 * (E.cy - N / 2)
+    ref = P.linogram_of_ellipses(E, N).numpy()
+    sino = P.sinogram_of_ellipses(E, N, 4 * N, int(math.ceil(N * math.sqrt(2) / 0.5)) + 4, 0.5).numpy()
+    S = O.resample_sinogram(sino, N, 0.5)
+    assert math.sqrt(((S - ref) ** 2).mean()) / math.sqrt((ref ** 2).mean()) < 0.02
