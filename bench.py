@@ -289,6 +289,41 @@ def run_fbp(args):
                             "achieved": alg_f * B * kf / (ms_f / 1e3) / 1e9}}
         del lin_f
 
+    # ---- NEXT-2: sinogram -> linogram resampling (fbp_resample_sinogram, Eq.14-15) ----
+    rsm = None
+    if not args.no_forward:
+        import math
+        na, dr = 2 * N, 1.0
+        nb = int(math.ceil(math.sqrt(2) * N / dr)) + 4
+        E = phantoms.draw_ellipses(N, 50, (N / 128, N / 3.2), seed=1000 * CFG + rank * B)
+        sino1 = phantoms.sinogram_of_ellipses(E, N, na, nb, dr).to(torch.float32).to(dev)
+        sino = sino1.unsqueeze(0).repeat(B, 1, 1).contiguous()
+        del sino1
+        lin_r = torch.empty_like(S)
+        for _ in range(3):
+            plan.resample(sino, dr=dr, out=lin_r, stream=stream)
+        kr = max(1, min(args.steps, 20))
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0.record(stream)
+        for _ in range(kr):
+            plan.resample(sino, dr=dr, out=lin_r, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms_r = e0.elapsed_time(e1)
+        tr = torch.tensor([ms_r], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+        ms_r = float(tr[0])
+        alg_r = 4.0 * na * nb + 32.0 * N * N        # sinogram read + linogram write
+        rsm = {"value": world * B * kr / (ms_r / 1e3), "unit": UNIT, "steps": kr, "ms_per_step": ms_r / kr,
+               "input": f"analytic 50-ellipse sinogram, {na} angles x {nb} bins, dr={dr}",
+               "gpu_launches_per_step": plan.launch_count(),
+               "roofline": {"bound": "hbm", "alg_bytes_per_slice": alg_r, "unit": "GB/s per GPU",
+                            "achieved": alg_r * B * kr / (ms_r / 1e3) / 1e9}}
+        del lin_r, sino
+
     # ---- end to end through the public host-buffer C-ABI call ----
     e2e = None
     if not args.no_e2e:
@@ -354,10 +389,14 @@ def run_fbp(args):
             "clocks": clocks,
             "e2e": e2e,
         }
-        if fwd is not None:
-            fwd["roofline"]["peak"] = peak
-            fwd["roofline"]["frac"] = fwd["roofline"]["achieved"] / peak
-            line["next"] = {"fht_forward": fwd}
+        nxt = {}
+        for key, item in (("fht_forward", fwd), ("resample", rsm)):
+            if item is not None:
+                item["roofline"]["peak"] = peak
+                item["roofline"]["frac"] = item["roofline"]["achieved"] / peak
+                nxt[key] = item
+        if nxt:
+            line["next"] = nxt
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(N, b, a)
         print(json.dumps(line), flush=True)
@@ -378,7 +417,7 @@ def main():
     ap.add_argument("--e2e-batch", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-forward", action="store_true", help="skip the NEXT-1 forward-FHT line item")
+    ap.add_argument("--no-forward", action="store_true", help="skip the NEXT-1/NEXT-2 line items (forward FHT, resampling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -111,6 +111,24 @@ FBP_API fbp_status fbp_fht_forward(const fbp_plan* plan, const float* image, flo
                                    void* cuda_stream);
 
 /*
+ * fbp_resample_sinogram -- scanner sinogram -> linogram (NEXT-2), the step before
+ * the hot path:                                        PAPER.md:172-188 (Eq.14-15)
+ *   sino: device [batch][n_angles][n_bins] fp32, p(r_j, theta_k) with theta_k =
+ *         k*pi/n_angles the angle of the line normal (cos, sin) in image coordinates
+ *         (x = column, y = row) and r_j = (j - (n_bins-1)/2)*dr the signed distance
+ *         from the image centre (N/2, N/2) (reading R23);
+ *   lin:  device [batch][4][N][2N] (overwritten): sample (f, t, s) = the sinogram
+ *         linearly interpolated (angle and bin index; the row after the last angle
+ *         is row 0 at -r; bins outside the detector read 0) at the (r, theta) of
+ *         its line (Eq.14 for the line model of reading R2), divided by the Eq.15
+ *         stretch sqrt(1 + (t/(N-1))^2) of that line.
+ *   Errors: FBP_ERR_PARAM (NULL / misaligned pointer, batch outside [0, max_batch],
+ *   n_angles or n_bins < 1, dr not finite and > 0), FBP_ERR_CUDA.
+ */
+FBP_API fbp_status fbp_resample_sinogram(const fbp_plan* plan, const float* sino, int n_angles, int n_bins,
+                                         double dr, float* lin, int batch, void* cuda_stream);
+
+/*
  * fbp_reconstruct -- the whole hot path: IIR ramp filter then FHT back
  * projection with weight w = 1/N (reading R7).
  *   sino: device [batch][4][N][2N];  image: device [batch][N][N].
@@ -147,9 +165,9 @@ FBP_API long long fbp_plan_launch_count(const fbp_plan* plan);
  * every kernel while enabled).  fbp_plan_profile(plan, 1) clears and enables,
  * 0 disables.  fbp_plan_kernel_times synchronises on the recorded events and
  * writes, for kind k in {0: IIR, 1: FHT pass A, 2: FHT pass B, 3: forward FHT
- * pass A, 4: forward FHT pass B}, the summed milliseconds ms[k] and launch count
- * launches[k] (arrays of length `kinds`, at most 5) since the last enable, then
- * clears the record.
+ * pass A, 4: forward FHT pass B, 5: sinogram resampling}, the summed milliseconds
+ * ms[k] and launch count launches[k] (arrays of length `kinds`, at most 6) since
+ * the last enable, then clears the record.
  */
 FBP_API fbp_status fbp_plan_profile(fbp_plan* plan, int enable);
 FBP_API fbp_status fbp_plan_kernel_times(fbp_plan* plan, double* ms, long long* launches, int kinds);

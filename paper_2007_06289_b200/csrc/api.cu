@@ -544,6 +544,32 @@ fbp_status fbp_fht_forward(const fbp_plan* p, const float* image, float* lin, in
   return FBP_OK;
 }
 
+fbp_status fbp_resample_sinogram(const fbp_plan* p, const float* sino, int n_angles, int n_bins, double dr,
+                                 float* lin, int batch, void* stream) {
+  fbp_status s = check_call(p, sino, lin, batch);
+  if (s != FBP_OK || batch == 0) return s;
+  if (n_angles < 1 || n_bins < 1) return fail(FBP_ERR_PARAM, "n_angles and n_bins must be >= 1");
+  if (!(dr > 0.0) || !std::isfinite(dr)) return fail(FBP_ERR_PARAM, "dr must be finite and > 0");
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  const long long lin_elems = 4LL * p->g.N * p->g.W;
+  const long long sino_elems = (long long)n_angles * n_bins;
+  const cudaStream_t st = (cudaStream_t)stream;
+  for (int s0 = 0; s0 < batch; s0 += 16383) {
+    const int ns = std::min(16383, batch - s0);
+    cudaError_t e = timed(p, 5, st, [&] {
+      return launch_resample(sino + s0 * sino_elems, lin + s0 * lin_elems, ns, n_angles, n_bins, dr, p->g, st,
+                             &launches);
+    });
+    if (e != cudaSuccess) {
+      p->launches = launches;
+      return cuda_fail(e, "fbp_resample_sinogram");
+    }
+  }
+  p->launches = launches;
+  return FBP_OK;
+}
+
 fbp_status fbp_reconstruct(const fbp_plan* p, const float* sino, float* image, int batch,
                            void* stream) {
   fbp_status s = check_call(p, sino, image, batch);
@@ -680,7 +706,7 @@ fbp_status fbp_plan_profile(fbp_plan* p, int enable) {
 }
 
 fbp_status fbp_plan_kernel_times(fbp_plan* p, double* ms, long long* launches, int kinds) {
-  if (!p || kinds < 0 || kinds > 5 || (kinds > 0 && (!ms || !launches)))
+  if (!p || kinds < 0 || kinds > 6 || (kinds > 0 && (!ms || !launches)))
     return fail(FBP_ERR_PARAM, "fbp_plan_kernel_times: bad arguments");
   DeviceGuard guard(p->device);
   for (int k = 0; k < kinds; ++k) {

@@ -102,6 +102,10 @@ cudaError_t launch_fht_pass_b(const float* R, float* img, int slices, int pair, 
 // Forward FHT (fwd.cu, Eq.17): image [slices][N][N] -> R_A (workspace of
 // fwd_workspace_floats per slice) -> linogram [slices][4][N][2N].  slices <= 16383.
 size_t fwd_workspace_floats(const Geometry& g);
+// Sinogram -> linogram (resample.cu, Eq.14-15, R23): sino [slices][n_angles][n_bins]
+// -> lin [slices][4][N][2N].  slices <= 16383.
+cudaError_t launch_resample(const float* sino, float* lin, int slices, int n_angles, int n_bins, double dr,
+                            const Geometry& g, cudaStream_t st, int* launches);
 cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry& g, cudaStream_t st,
                          int* launches);
 cudaError_t launch_fwd_b(const float* RA, float* lin, int slices, const Geometry& g, cudaStream_t st,

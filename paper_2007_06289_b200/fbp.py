@@ -9,6 +9,7 @@ missing or the device is not an sm_100 B200 it raises.
     F    = plan.iir_filter(sino)             # Eq.12-13
     bp   = plan.backproject(F, scale=1/N)    # Eq.19-22
     lin  = plan.forward(img)                 # Eq.17 (forward FHT)
+    lin  = plan.resample(sino_rtheta, dr=1)  # Eq.14-15 (scanner sinogram -> linogram)
 """
 from __future__ import annotations
 
@@ -25,11 +26,11 @@ FBP_STATUS = {0: "FBP_OK", 1: "FBP_ERR_PLAN", 2: "FBP_ERR_PARAM", 3: "FBP_ERR_UN
               4: "FBP_ERR_CUDA", 5: "FBP_ERR_NOMEM", 6: "FBP_ERR_DEVICE"}
 
 EXPORTED = ["fbp_plan_create", "fbp_plan_destroy", "fbp_iir_filter", "fbp_fht_backproject",
-            "fbp_fht_forward", "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
+            "fbp_fht_forward", "fbp_resample_sinogram", "fbp_reconstruct", "fbp_reconstruct_host", "fbp_status_str", "fbp_last_error",
             "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_path", "fbp_plan_profile",
             "fbp_plan_kernel_times"]
 
-KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b", "fwd_pass_a", "fwd_pass_b")
+KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b", "fwd_pass_a", "fwd_pass_b", "resample")
 
 
 class FbpError(RuntimeError):
@@ -57,6 +58,8 @@ def lib():
     L.fbp_fht_backproject.restype = i
     L.fbp_fht_forward.argtypes = [vp, vp, vp, i, vp]
     L.fbp_fht_forward.restype = i
+    L.fbp_resample_sinogram.argtypes = [vp, vp, i, i, ctypes.c_double, vp, i, vp]
+    L.fbp_resample_sinogram.restype = i
     L.fbp_reconstruct.argtypes = [vp, vp, vp, i, vp]
     L.fbp_reconstruct.restype = i
     L.fbp_reconstruct_host.argtypes = [vp, vp, vp, i]
@@ -200,6 +203,24 @@ class Plan:
         else:
             out = self._lin(out, "out")
         _check(lib().fbp_fht_forward(self._h, image.data_ptr(), out.data_ptr(), B, _stream_ptr(stream)))
+        return out
+
+    def resample(self, sino: torch.Tensor, dr: float = 1.0, out: torch.Tensor | None = None, stream=None):
+        """Scanner sinogram [B, n_angles, n_bins] -> linogram [B, 4, N, 2N] (Eq.14-15)."""
+        N = self.n
+        if not (isinstance(sino, torch.Tensor) and sino.is_cuda and sino.dtype == torch.float32):
+            raise TypeError("sino must be a float32 CUDA tensor")
+        if sino.dim() == 2:
+            sino = sino.unsqueeze(0)
+        if sino.dim() != 3 or not sino.is_contiguous():
+            raise ValueError(f"sino must be a contiguous [B, n_angles, n_bins] tensor, got {tuple(sino.shape)}")
+        B, na, nb = sino.shape
+        if out is None:
+            out = torch.empty((B, 4, N, 2 * N), device=sino.device, dtype=torch.float32)
+        else:
+            out = self._lin(out, "out")
+        _check(lib().fbp_resample_sinogram(self._h, sino.data_ptr(), na, nb, float(dr), out.data_ptr(), B,
+                                           _stream_ptr(stream)))
         return out
 
     def reconstruct(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):

@@ -24,7 +24,7 @@ def header_symbols():
 
 def test_exports_every_declared_symbol(L):
     syms = header_symbols()
-    assert len(syms) == 14, syms
+    assert len(syms) == 15, syms
     for s in syms:
         assert hasattr(L, s), s
     from paper_2007_06289_b200 import fbp

@@ -362,3 +362,80 @@ def test_forward_edge_cases(fbp):
     img[0, 5, 9] = 1.0
     S = plan.forward(img).cpu().numpy()[0]
     assert np.all(S.sum(axis=2) == 1.0) and np.all((S == 1.0).sum(axis=2) == 1)
+
+
+# ------------------------------------------------ sinogram resampling (NEXT-2)
+def _ellipse_sinogram(N, n_angles, dr, seed):
+    import math
+    E = P.draw_ellipses(N, 12, (N / 32, N / 6), seed=seed)
+    nb = int(math.ceil(math.sqrt(2) * N / dr)) + 4
+    return E, P.sinogram_of_ellipses(E, N, n_angles, nb, dr).to(torch.float32)
+
+
+@pytest.mark.parametrize("N,na,nb,dr", [(16, 32, 27, 1.0), (64, 193, 50, 0.7), (64, 256, 186, 0.5)])
+def test_resample_matches_oracle(fbp, N, na, nb, dr):
+    """fbp_resample_sinogram vs oracle resample_sinogram on the same fp32 sinogram,
+    every sample (random values, odd geometries, detector narrower than the image)."""
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    g = torch.Generator().manual_seed(N + na)
+    sino = torch.rand((2, na, nb), generator=g, dtype=torch.float32)
+    out = plan.resample(sino.cuda(), dr=dr).cpu().numpy()
+    for i in range(2):
+        ref = O.resample_sinogram(sino[i].double().numpy(), N, dr)
+        assert rel_err(out[i], ref) <= 1e-5, i
+
+
+def test_resample_full_size_sampled(fbp):
+    """N = 2048 (config-3 size, 2N angles, unit bins): sampled outputs vs the oracle's
+    per-sample definition, and the GPU result close to the analytic linogram."""
+    import math
+    N, na, dr = 2048, 4096, 1.0
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    E, sino = _ellipse_sinogram(N, na, dr, seed=7)
+    out = plan.resample(sino.cuda(), dr=dr).cpu().numpy()[0]
+    sn = sino.double().numpy()
+    peak = float(np.abs(out).max())
+    rng = np.random.default_rng(1)
+    for _ in range(40):
+        f, t, s_ = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+        r, th, L = O.linogram_line_rtheta(f, t, s_, N)
+        ref = O.sinogram_sample(sn, th, r, dr) / L
+        assert abs(float(out[f, t, s_]) - ref) <= 1e-5 * peak, (f, t, s_)
+
+
+def test_resample_close_to_analytic_linogram(fbp):
+    """GPU resampling of an analytic sinogram reproduces the analytic linogram of the
+    same ellipses (ellipses inside the square) within interpolation error (N = 256)."""
+    import math
+    N, na, dr = 256, 1024, 0.5
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    E = P.draw_ellipses(N, 12, (N / 32, N / 6), seed=3)
+    E.cx = N / 2 + 0.5 * (E.cx - N / 2)
+    E.cy = N / 2 + 0.5 * (E.cy - N / 2)
+    nb = int(math.ceil(math.sqrt(2) * N / dr)) + 4
+    sino = P.sinogram_of_ellipses(E, N, na, nb, dr).to(torch.float32)
+    out = plan.resample(sino.cuda(), dr=dr).cpu().numpy()[0]
+    ref = P.linogram_of_ellipses(E, N).numpy()
+    assert math.sqrt(((out - ref) ** 2).mean()) / math.sqrt((ref ** 2).mean()) < 0.01
+
+
+def test_resample_edge_cases(fbp):
+    N = 16
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=2)
+    z = plan.resample(torch.zeros((0, 8, 8), device="cuda"))
+    assert z.shape == (0, 4, N, 2 * N)
+    with pytest.raises(fbp.FbpError):
+        plan.resample(torch.zeros((1, 8, 8), device="cuda"), dr=0.0)
+    with pytest.raises(fbp.FbpError):
+        plan.resample(torch.zeros((3, 8, 8), device="cuda"))          # batch > max_batch
+    # a zero sinogram gives a zero linogram; a constant sinogram gives 1/|D| on every
+    # line through the square: s >= N puts (x0 + 0.5, 0.5) inside it, so |r| <= N/sqrt(2)
+    # lies within the 40-bin detector
+    assert not plan.resample(torch.zeros((1, 8, 40), device="cuda")).any()
+    out = plan.resample(torch.ones((1, 8, 40), device="cuda")).cpu().numpy()[0]
+    for t in (0, 7, N - 1):
+        assert np.allclose(out[:, t, N:], 1.0 / np.sqrt(1.0 + (t / (N - 1)) ** 2), rtol=1e-6)
