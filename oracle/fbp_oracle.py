@@ -19,7 +19,8 @@ Notation:
     G_3 = img[N-1-x][y]  (Eq.16 transpose + mirror for the shift sign, R4).
 
 Pinned by ``tests/test_oracle_pins.py`` (closed forms, SPEC worked examples,
-library routines, brute force, exact adjoint identities).  Parity status per
+library routines, brute force, exact adjoint identities; the NEXT-2 resampling
+against the phantom generator's own line model and analytic linograms).  Parity status per
 function is listed in DESIGN.md §4; nothing here is "parity unpinned" except the
 numeric values of the paper's own (unprinted) IIR coefficients, which are an
 input, not a computation.
