@@ -10,10 +10,10 @@
 //
 // One CTA per linogram row (t, family, slice): thread 0 derives the row's geometry
 // once in double precision (theta, the angle weight, r as an affine function of s,
-// 1/|D|); the threads sweep s, evaluating the bin position in double (|r| reaches
-// ~1.5 N, so fp32 would leave ~1e-4-bin errors at N = 2048) and interpolating in
-// fp32.  HBM-bound: writes 32 N^2 B per slice, reads two sinogram rows per
-// linogram row (mostly from L2).
+// 1/|D|); each thread takes four consecutive s, evaluating the bin position of the
+// first in double (|r| reaches ~1.5 N, so an fp32 position would be off by ~1e-4
+// bins at N = 2048) and interpolating in fp32.  HBM-bound in principle: writes
+// 32 N^2 B per slice, reads two sinogram rows per linogram row (mostly from L2).
 #include <cmath>
 
 #include "fbp_internal.h"
@@ -32,10 +32,9 @@ struct RowGeo {
   int k0, k1;    // angle rows; k1 = -1: row 0 at -r
 };
 
-__device__ __forceinline__ float interp_row(const float* __restrict__ row, int R, double w) {
-  const double fl = floor(w);
-  const int j0 = (int)fl;
-  const float b = (float)(w - fl);
+// Linear interpolation of one sinogram row at bin position j + b (b in [0, 1) up to
+// rounding; bins outside [0, R) read 0).
+__device__ __forceinline__ float interp_row(const float* __restrict__ row, int R, int j0, float b) {
   float v = 0.f;
   if (j0 >= 0 && j0 < R) v += (1.f - b) * __ldg(row + j0);
   if (j0 + 1 >= 0 && j0 + 1 < R) v += b * __ldg(row + j0 + 1);
@@ -85,11 +84,33 @@ __global__ void __launch_bounds__(RNT) k_resample(const float* __restrict__ sino
   const float* row1 = ps + (long long)(geo.k1 >= 0 ? geo.k1 : 0) * R;
   const bool wrap = geo.k1 < 0;
   float* out = lin + ((long long)sf * N + t) * (2 * N);
-  for (int s = threadIdx.x; s < 2 * N; s += RNT) {
-    const double w = geo.w0 + s * geo.dw;
-    const float v0 = interp_row(row0, R, w);
-    const float v1 = interp_row(row1, R, wrap ? geo.wf0 - s * geo.dw : w);
-    out[s] = ((1.f - a) * v0 + a * v1) * il;
+  const float dwf = (float)geo.dw;
+  // 4 consecutive s per thread (float4 store): the bin position of the quad's first
+  // sample in fp64, the next three as fp32 offsets from its integer part (< 4 bins)
+  for (int q0 = 4 * threadIdx.x; q0 < 2 * N; q0 += 4 * RNT) {
+    const double w = geo.w0 + q0 * geo.dw;
+    const double wfl = floor(w);
+    const int jw = (int)wfl;
+    const float fw = (float)(w - wfl);
+    const double x = geo.wf0 - q0 * geo.dw;           // wrapped row: row 0 at -r
+    const double xfl = floor(x);
+    const int jx = (int)xfl;
+    const float fx = (float)(x - xfl);
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float pw = fw + q * dwf, fpw = floorf(pw);
+      const float v0 = interp_row(row0, R, jw + (int)fpw, pw - fpw);
+      float v1;
+      if (wrap) {
+        const float px = fx - q * dwf, fpx = floorf(px);
+        v1 = interp_row(row1, R, jx + (int)fpx, px - fpx);
+      } else {
+        v1 = interp_row(row1, R, jw + (int)fpw, pw - fpw);
+      }
+      o[q] = ((1.f - a) * v0 + a * v1) * il;
+    }
+    *reinterpret_cast<float4*>(out + q0) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
