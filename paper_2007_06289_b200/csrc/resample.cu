@@ -8,7 +8,7 @@
 // (row after P-1 = row 0 at -r) and in the bin index (bins outside [0, R) read 0),
 // and the value is divided by the Eq.15 stretch |D| = sqrt(1 + k^2) of that line.
 //
-// One CTA per linogram row (t, family, slice): thread 0 derives the row's geometry
+// One CTA per linogram row (t, family) and group of up to 16 slices: thread 0 derives the row's geometry
 // once in double precision (theta, the angle weight, r as an affine function of s,
 // 1/|D|); each thread takes four consecutive s, evaluating the bin position of the
 // first in double (|r| reaches ~1.5 N, so an fp32 position would be off by ~1e-4
@@ -41,11 +41,13 @@ __device__ __forceinline__ float interp_row(const float* __restrict__ row, int R
   return v;
 }
 
-// grid (N rows t, 4 * slices)
+// grid (N rows t, 4 families, slice groups of SPB): the row geometry does not depend
+// on the slice, so each CTA derives it once and sweeps its slices
+constexpr int SPB = 16;
 __global__ void __launch_bounds__(RNT) k_resample(const float* __restrict__ sino, float* __restrict__ lin,
-                                                  int N, int P, int R, double dr) {
+                                                  int N, int P, int R, double dr, int slices) {
   __shared__ RowGeo geo;
-  const int t = blockIdx.x, sf = blockIdx.y, f = sf & 3;
+  const int t = blockIdx.x, f = blockIdx.y;
   if (threadIdx.x == 0) {
     const double k = (double)t / (N - 1);
     const double A0 = -N + 0.5 - 0.5 * k;              // A at s = 0
@@ -79,12 +81,14 @@ __global__ void __launch_bounds__(RNT) k_resample(const float* __restrict__ sino
   }
   __syncthreads();
   const float a = (float)geo.a, il = geo.inv_len;
-  const float* ps = sino + (long long)(sf >> 2) * P * R;
+  const bool wrap = geo.k1 < 0;
+  const float dwf = (float)geo.dw;
+  const int sl_end = min(slices, (int)(blockIdx.z + 1) * SPB);
+  for (int sl = blockIdx.z * SPB; sl < sl_end; ++sl) {
+  const float* ps = sino + (long long)sl * P * R;
   const float* row0 = ps + (long long)geo.k0 * R;
   const float* row1 = ps + (long long)(geo.k1 >= 0 ? geo.k1 : 0) * R;
-  const bool wrap = geo.k1 < 0;
-  float* out = lin + ((long long)sf * N + t) * (2 * N);
-  const float dwf = (float)geo.dw;
+  float* out = lin + ((long long)(sl * 4 + f) * N + t) * (2 * N);
   // 4 consecutive s per thread (float4 store): the bin position of the quad's first
   // sample in fp64, the next three as fp32 offsets from its integer part (< 4 bins)
   for (int q0 = 4 * threadIdx.x; q0 < 2 * N; q0 += 4 * RNT) {
@@ -112,14 +116,15 @@ __global__ void __launch_bounds__(RNT) k_resample(const float* __restrict__ sino
     }
     *reinterpret_cast<float4*>(out + q0) = make_float4(o[0], o[1], o[2], o[3]);
   }
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_resample(const float* sino, float* lin, int slices, int n_angles, int n_bins, double dr,
                             const Geometry& g, cudaStream_t st, int* launches) {
-  const dim3 grid(g.N, 4 * slices);
-  k_resample<<<grid, RNT, 0, st>>>(sino, lin, g.N, n_angles, n_bins, dr);
+  const dim3 grid(g.N, 4, (slices + SPB - 1) / SPB);
+  k_resample<<<grid, RNT, 0, st>>>(sino, lin, g.N, n_angles, n_bins, dr, slices);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
