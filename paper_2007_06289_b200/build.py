@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+# developer builds only, e.g. FBP_NVCC_FLAGS=-DFBP_DEV_MASK=1 (timing skip mask)
+FLAGS += os.environ.get("FBP_NVCC_FLAGS", "").split()
 
 
 def sources():

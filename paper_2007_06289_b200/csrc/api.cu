@@ -407,10 +407,6 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
       put(si.M2, 64);
       put(si.MX, sg.X);
       put(si.M16, 16);
-      for (int i = 0; i < 32; ++i) {
-        matpow(3, A3, i + 1, Pm);
-        for (int mm = 0; mm < 3; ++mm) si.G[i][mm] = dup(Pm[(size_t)mm]);
-      }
       p->fast = true;
     }
   }

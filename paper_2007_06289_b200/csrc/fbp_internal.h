@@ -56,7 +56,6 @@ struct SweepIir {
   float2 M2[9];               // A^64
   float2 MX[9];               // A^X   (one tile)
   float2 M16[9];              // A^16
-  float2 G[32][3];            // G[i][m] = (A^(i+1))_{0m}
 };
 
 struct SweepGeom {
@@ -67,7 +66,8 @@ struct SweepGeom {
   int P;      // pass-B L2 prefetch distance in items (env FBP_PREFETCH)
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
-  int dbg;    // developer timing mask, env FBP_DBG (results invalid when nonzero): pass B bit 0
+  int dbg;    // developer timing mask, env FBP_DBG, honoured only in -DFBP_DEV_MASK=1 builds
+              // (results invalid when nonzero): pass B bit 0
               // skips the FHT steps, bit 1 the epilogue, bit 2 the fills; sweep bit 3
               // skips every TMA load
 };

@@ -36,6 +36,12 @@
 
 #include <algorithm>
 
+// Developer timing mask (env FBP_DBG, tools/dev_timing.py: skip TMA loads / FHT
+// steps / epilogue to attribute time) -- compiled in only with -DFBP_DEV_MASK=1.
+#ifndef FBP_DEV_MASK
+#define FBP_DEV_MASK 0
+#endif
+
 namespace fbp {
 
 namespace {
@@ -354,6 +360,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 
   const int tid = threadIdx.x;
   const int D = g.D;
+  const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
   using HT = HaloTab<H, HS, O2, PS, NT>;
   unsigned hoff[HT::NKH];                                // this thread's S1 halo quads
 #pragma unroll
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     //   look-ahead: box of H rows x PL columns from column jt*X
     const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
     auto tma_issue = [&](const CUtensorMap* mp, int ob, int col, unsigned bytes, int bi) {
-      if (tid == 0 && !(g.dbg & 8)) {
+      if (tid == 0 && !(dbgm & 8)) {
         fence_proxy_async();
         const unsigned bar = smem_u32(oBar + 2 * bi);
         mbar_expect_tx(bar, bytes);
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       }
     };
     auto tma_wait = [&](int bi) {
-      if (!(g.dbg & 8)) mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
+      if (!(dbgm & 8)) mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
       ph ^= 1u << bi;
     };
     auto land = [&](int jt) { tma_issue(&tmapF, oF, jt * X - 8, H * PF * 4, 0); };
@@ -773,6 +780,7 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
   static_assert(2 * NB * PK <= 2 * NB * PI, "park must fit in the input buffer");
   const int N = g.N, H = g.H;
   const int tid = threadIdx.x;
+  const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
   const int nx = (N + XB - 1) / XB;
   constexpr int oBar = oG0 + NBUF * G_SZ;             // NBUF mbarriers (8-byte aligned)
   if (tid == 0) {
@@ -789,7 +797,7 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
   const PbPos step = pb_pos(gridDim.x, nx, H);
   const PbPos stepP = pb_pos((long long)g.P * gridDim.x, nx, H);
   auto issue = [&](const PbPos& pt, int bb) {
-    if (tid != 0 || pt.sl >= nsl || (g.dbg & 4)) return;
+    if (tid != 0 || pt.sl >= nsl || (dbgm & 4)) return;
     if (g.P > 0) {
       const PbPos pp = pb_add(pt, stepP, nx, H);
       if (pp.sl < nsl) {
@@ -826,10 +834,10 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
     // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
     //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
     //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
-    if (!(g.dbg & 4)) mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);   // bit 2: do not wait (timing only)
+    if (!(dbgm & 4)) mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);
     ph ^= 1u << bb;
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
-    if (!(g.dbg & 1)) {
+    if (!(dbgm & 1)) {
       constexpr int nch = (HS + XB) / C1;
       constexpr int per_fam = (NB / NR1) * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
@@ -849,7 +857,7 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
     }
     __syncthreads();
     // ---- step 2: both families, core columns -> park (aliasing the input) ----
-    if (!(g.dbg & 1)) {
+    if (!(dbgm & 1)) {
       constexpr int nch = XB / C2;
       constexpr int per_fam = NR1 * nch;
       for (int it = tid; it < 2 * per_fam; it += NT) {
@@ -876,7 +884,7 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
     }
     __syncthreads();
     // ---- epilogue ----
-    if (g.dbg & 2) {
+    if (dbgm & 2) {
     } else if (PAIR == 0) {
       constexpr int nq = XB / 4;
       float* const outc = img + ((long long)cur.sl * N + ch * NB) * N + x0;   // image rows ch*NB..
