@@ -76,6 +76,30 @@ def test_backproject_integer_bit_exact_sampled_full_size(fbp, N):
         assert float(out[y, x]) == ref, (N, y, x)
 
 
+def test_backproject_and_forward_max_size_8192(fbp):
+    """The plan's maximum N = 8192 (general path, k1 = 7, m = 6): sampled BP pixels and
+    forward samples exact on integers (|values| <= 255 keeps every sum below 2^24)."""
+    N = 8192
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    lin = P.integer_linogram(N, 1, seed=8192, lo=-255, hi=255)
+    out = plan.backproject(lin.cuda(), scale=1.0).cpu().numpy()[0]
+    L = lin[0].numpy()
+    del lin
+    rng = np.random.default_rng(N)
+    for (y, x) in [(0, 0), (N - 1, N - 1)] + [tuple(rng.integers(0, N, 2)) for _ in range(6)]:
+        ref = (O.backproject_pixel(L, 0, y, x) + O.backproject_pixel(L, 1, y, N - 1 - x)
+               + O.backproject_pixel(L, 2, x, y) + O.backproject_pixel(L, 3, x, N - 1 - y))
+        assert float(out[y, x]) == ref, (y, x)
+    del L, out
+    img = P.integer_image(N, 1, seed=5, lo=-255, hi=255)
+    S = plan.forward(img.cuda()).cpu().numpy()[0]
+    im = img[0].numpy().astype(np.float64)
+    for _ in range(6):
+        f, t, s_ = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+        assert float(S[f, t, s_]) == O.forward_sample(im, f, t, s_), (f, t, s_)
+
+
 def test_backproject_float_random(fbp):
     N = 256
     b, a = coeffs(N)
@@ -372,7 +396,7 @@ def _ellipse_sinogram(N, n_angles, dr, seed):
     return E, P.sinogram_of_ellipses(E, N, n_angles, nb, dr).to(torch.float32)
 
 
-@pytest.mark.parametrize("N,na,nb,dr", [(16, 32, 27, 1.0), (64, 193, 50, 0.7), (64, 256, 186, 0.5)])
+@pytest.mark.parametrize("N,na,nb,dr", [(2, 4, 5, 1.0), (16, 32, 27, 1.0), (64, 193, 50, 0.7), (64, 256, 186, 0.5)])
 def test_resample_matches_oracle(fbp, N, na, nb, dr):
     """fbp_resample_sinogram vs oracle resample_sinogram on the same fp32 sinogram,
     every sample (random values, odd geometries, detector narrower than the image)."""
