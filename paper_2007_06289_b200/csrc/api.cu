@@ -361,6 +361,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.XB = (sg.NB == 32) ? 64 : 128;
     if (const char* ev = std::getenv("FBP_XB")) sg.XB = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
+    if (const char* ev = std::getenv("FBP_SWEEP_SEG")) sg.nseg = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_DBG")) sg.dbg = std::atoi(ev);
     // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
     const int K = 1 << 16;

@@ -66,6 +66,7 @@ struct SweepGeom {
   int P;      // pass-B L2 prefetch distance in items (env FBP_PREFETCH)
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
+  int nseg;   // segments per sweep (0: automatic, fill the CTA slots); env FBP_SWEEP_SEG
   int dbg;    // developer timing mask, env FBP_DBG, honoured only in -DFBP_DEV_MASK=1 builds
               // (results invalid when nonzero): pass B bit 0
               // skips the FHT steps, bit 1 the epilogue, bit 2 the fills; sweep bit 3

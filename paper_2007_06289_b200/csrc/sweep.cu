@@ -340,7 +340,7 @@ __device__ constexpr HaloTab<H, HS, O2, PS, NT> kHaloTab{};
 template <int H, int X, bool IIR, bool BETA>
 __global__ void __launch_bounds__(H * X / 32, 3)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
-              int slices, int f0, int nf, long long lin_slice_stride, int* __restrict__ counter,
+              int slices, int f0, int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
               const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapL) {
   constexpr int NT = H * X / 32;
   constexpr int TPR = X / 32;                 // chunks (threads) per row in the IIR
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   unsigned ph = 0;                                       // phase bits of the 3 mbarriers
   const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
   const long long nsf = (long long)slices * nf;
-  const long long nitems = nsf * NB;
+  const long long nitems = nsf * NB * nseg;
   // IIR roles: a quarter-warp = 8 rows x the same chunk (conflict-free), the TPR
   // chunks of a row sit 8 lanes apart in one warp.
   const int iq = (tid >> 3) % TPR;
@@ -390,8 +390,12 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     __syncthreads();
     const long long item = *s_item;
     if (item >= nitems) break;
-    const int b = NB - 1 - (int)(item / nsf);            // longest sweeps first
-    const long long sfi = item - (long long)(NB - 1 - b) * nsf;
+    // item = (block b, slice*family, segment): longest sweeps first, a sweep's
+    // segments adjacent
+    const int seg = (int)(item % nseg);
+    const long long it2 = item / nseg;
+    const int b = NB - 1 - (int)(it2 / nsf);
+    const long long sfi = it2 - (long long)(NB - 1 - b) * nsf;
     const long long s = sfi / nf;
     const int fi = (int)(sfi - s * nf);
     const int f = f0 + fi;
@@ -406,7 +410,16 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     // anticausal look-ahead (R22); linogram rows need not be zero left of N - t
     // (noisy inputs, configs 2, 4, 5).
     const int j0 = (N - (b + 1) * H + 1) / X;
-    const int jst = IIR ? max(0, j0 - D) : j0;
+    // Segments (small batches, more CTAs than sweeps): segment seg stores the tiles
+    // [ja, jb) of [j0, nt).  It runs step 1 from j1 = ja - 1 (the S1 halo of tile ja
+    // is tile ja - 1's step-1 output; segment 0 needs none, as above) and its IIR
+    // from D tiles before j1 -- the same warm-up / look-ahead bound (R22) as the
+    // sweep's first tile.
+    const int seglen = (nt - j0 + nseg - 1) / nseg;
+    const int ja = j0 + seg * seglen, jb = min(nt, ja + seglen);
+    if (ja >= jb) continue;
+    const int j1 = (seg == 0) ? j0 : ja - 1;
+    const int jst = IIR ? max(0, j1 - D) : j1;
 
     // TMA landings (thread 0 issues; every thread waits on the mbarrier):
     //   F tile : box of H rows x PF columns from column jt*X - 8 (halo room, left
@@ -498,7 +511,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     }
     int slot_j = 0;                                    // ring slot of tile j (j - jst mod D+1)
 
-    for (int j = jst; j < nt; ++j) {
+    for (int j = jst; j < jb; ++j) {
       const int oFc = oF;
       const int jl = j + D + 1;
 
@@ -638,7 +651,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       __syncthreads();                                   // F tile complete
 
       // ---- FHT step 1 (levels 1-3): F -> S1 ----
-      if (j >= j0) {
+      if (j >= j1) {
         constexpr int NCH = X / C1;
         const int jj = tid % NCH, G = tid / NCH;
         float2 v[8][It<3, C1>::T / 2];
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
         st4(oStash + r * HF + 4 * qd, ld4(oFc + r * PF + X + 4 * qd));
       }
       __syncthreads();
-      if (j + 1 < nt) land(j + 1);                       // F is free: step 1 has read it
+      if (j + 1 < jb) land(j + 1);                       // F is free: step 1 has read it
       // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
       // Items whose NR2 channels cf = c*NR2 + r need none of their columns (u outside
       // [N - b(cf+1), 2N - cf*b) for every r) are skipped: up to half of them for
@@ -666,7 +679,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       constexpr int NCH2 = X / C2;
       const int ub2 = j * X + C2 * (tid % NCH2), c2 = tid / NCH2;
       const bool need2 = (ub2 + C2 > N - b * (c2 * NR2 + NR2)) && (ub2 < W - c2 * NR2 * b);
-      if (j >= j0 && need2) {
+      if (j >= ja && need2) {
         constexpr int NCH = X / C2;
         const int jj = tid % NCH, c = tid / NCH;
         float2 v[NR2][It<R2, C2>::T / 2];
@@ -701,7 +714,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
       // the needed (row, quad) pairs, dealt round-robin to the threads (HaloTab):
       // at most NKH live quads per thread, all loads issued before the stores
-      if (j >= j0) {
+      if (j >= j1) {
         float4 tq[HT::NKH];
 #pragma unroll
         for (int kk = 0; kk < HT::NKH; ++kk)
@@ -993,7 +1006,14 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, H * X / 32, smem);
   if (g.ctas_a > 0 && g.ctas_a < per) per = g.ctas_a;   // tuning knob (FBP_SWEEP_CTAS)
   if (per < 1) per = 1;
-  const long long nitems = (long long)slices * nf * g.NB;
+  // small batches: split every sweep into segments until there are ~1.7 work items
+  // per resident CTA slot (measured at N = 2048: B = 1 -> 6 segments, 2 -> 3, 4 -> 2,
+  // >= 8 -> 1; FBP_SWEEP_SEG overrides)
+  const long long sweeps = (long long)slices * nf * g.NB;
+  const long long slots = (long long)sms * per;
+  int nseg = (int)std::min<long long>(8, std::max<long long>(1, (17 * slots + 10 * sweeps - 1) / (10 * sweeps)));
+  if (g.nseg > 0) nseg = g.nseg;
+  const long long nitems = sweeps * nseg;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
   CUtensorMap tF, tL;
   e = make_lin_map(&tF, lin, slices, g, pitch4(8 + X + 4), H);
@@ -1001,7 +1021,7 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, counter, tF, tL);
+  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, nseg, counter, tF, tL);
   return cudaGetLastError();
 }
 
