@@ -12,7 +12,8 @@ if [ "${BENCH:-1}" = "1" ]; then
   echo "BENCH_EXIT=$?"; tail -3 gpurun_out/bench_${TAG}.log
 fi
 if [ "${NCU:-1}" = "1" ]; then
-  CMD="python bench.py --steps 2 --warmup 3 --batch 2 --no-e2e --no-cpu-baseline"
+  # capture at the bench's own batch (NCU_BATCH, default 16) so kernel shares match the bench line
+  CMD="python bench.py --steps 2 --warmup 3 --batch ${NCU_BATCH:-16} --no-e2e --no-cpu-baseline --no-forward"
   $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > /dev/null 2>&1
   echo "NCU_LAUNCHES=$?"
