@@ -84,8 +84,8 @@ def main():
     ap.add_argument("--report")
     ap.add_argument("--out", required=True)
     ap.add_argument("--json")
-    # tools/gpu_cycle.sh captures `bench.py --batch ${NCU_BATCH:-16}`: slices per launch
-    ap.add_argument("--slices-per-launch", type=float, default=16.0)
+    # tools/gpu_cycle.sh's --set full capture runs `bench.py --batch ${NCU_FULL_BATCH:-2}`
+    ap.add_argument("--slices-per-launch", type=float, default=2.0)
     ap.add_argument("--title", default="")
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
