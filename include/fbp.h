@@ -174,7 +174,7 @@ FBP_API fbp_status fbp_plan_kernel_times(fbp_plan* plan, double* ms, long long* 
 
 /*
  * Schedule chosen for this plan.  *fast = 1: fused IIR + FHT pass-A sweep and
- * pair-wise pass B (N in {512, 1024, 2048}, M <= 3, Q <= 3, coefficient tail
+ * pair-wise pass B (N in {512, 1024, 2048, 4096}, M <= 3, Q <= 3, coefficient tail
  * bound met); 0: separate IIR and two-pass FHT kernels.  *lookahead_tiles = D,
  * *tile_width = X of the sweep (0 when not fast).  Any pointer may be NULL.
  */

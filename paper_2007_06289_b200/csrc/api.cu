@@ -358,7 +358,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     if (const char* ev = std::getenv("FBP_PREFETCH")) sg.P = std::atoi(ev);
     // pass-B x-tile: 64 for NB = 32 (double-buffered TMA fills fit 2 CTAs/SM; measured
     // 5 % faster than 128 single-buffered), 128 otherwise
-    sg.XB = (sg.NB == 32) ? 64 : 128;
+    sg.XB = (sg.NB == 64) ? 32 : (sg.NB == 32) ? 64 : 128;   // NB = 64 (N = 4096): radix 8+8, single-buffered
     if (const char* ev = std::getenv("FBP_XB")) sg.XB = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_SWEEP_SEG")) sg.nseg = std::atoi(ev);

@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
 }
 
 // ---------------------------------------------------------------- host side
-bool sweep_supported(int N) { return N == 512 || N == 1024 || N == 2048; }
+bool sweep_supported(int N) { return N == 512 || N == 1024 || N == 2048 || N == 4096; }
 
 size_t sweep_a_smem(const SweepGeom& g) {
   const int H = g.H, X = g.X;
@@ -947,7 +947,7 @@ size_t sweep_a_smem(const SweepGeom& g) {
 }
 
 size_t pair_b_smem(const SweepGeom& g, int pair) {
-  const bool db = g.XB <= 64;
+  const bool db = g.XB <= 64 && g.NB <= 32;   // NB = 64: single buffer (2 CTAs/SM)
   const int NB = g.NB, XB = g.XB;
   int m = 0;
   while ((1 << m) < NB) ++m;
@@ -1051,7 +1051,7 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
 template <int R1, int R2, int XB, int PAIR>
 static cudaError_t launch_b_t(const float* R, float* img, int slices, float scale,
                               const SweepGeom& g, cudaStream_t st) {
-  auto kern = k_pair_b<R1, R2, XB, PAIR, (XB <= 64)>;
+  auto kern = k_pair_b<R1, R2, XB, PAIR, (XB <= 64 && R1 + R2 <= 5)>;
   const size_t smem = pair_b_smem(g, PAIR);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -1107,6 +1107,7 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
   FBP_PAIR_CASE(16, 2, 2, 128)
   FBP_PAIR_CASE(32, 3, 2, 128)
   FBP_PAIR_CASE(32, 3, 2, 64)
+  FBP_PAIR_CASE(64, 3, 3, 32)
 #undef FBP_PAIR_CASE
   if (launches) ++*launches;
   return e;

@@ -263,16 +263,17 @@ def _tail_lookahead(b, a, X, Dmax=16):
     return 0
 
 
-@pytest.mark.parametrize("N,variant", [(512, "dc0"), (1024, "spec"), (2048, "dc0"), (2048, "spec")])
+@pytest.mark.parametrize("N,variant", [(512, "dc0"), (1024, "spec"), (2048, "dc0"), (2048, "spec"),
+                                       (4096, "dc0")])
 def test_plan_path_fast(fbp, N, variant):
     b, a = coeffs(N, variant)
     p = fbp.Plan(N, b, a, max_batch=1).path()
-    X = 64 if N == 2048 else 128
+    X = 64 if N >= 2048 else 128
     assert p["fast"] and p["tile_width"] == X
     assert p["lookahead_tiles"] == _tail_lookahead(b, a, X)
 
 
-@pytest.mark.parametrize("N", [256, 4096])
+@pytest.mark.parametrize("N", [256, 8192])
 def test_plan_path_general(fbp, N):
     b, a = coeffs(N)
     assert not fbp.Plan(N, b, a, max_batch=1).path()["fast"]
@@ -280,7 +281,7 @@ def test_plan_path_general(fbp, N):
     assert not fbp.Plan(512, b + [0.0], a + [0.0], max_batch=1).path()["fast"]
 
 
-@pytest.mark.parametrize("N,cfg", [(512, 2), (2048, 3)])
+@pytest.mark.parametrize("N,cfg", [(512, 2), (2048, 3), (4096, 5)])
 def test_fast_path_matches_general_path(fbp, N, cfg):
     """The fused sweep (truncated carries, R22) and the exact general path are two
     independent implementations of the same filter; they agree to fp32 rounding."""
