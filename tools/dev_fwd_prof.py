@@ -1,3 +1,6 @@
+#!/usr/bin/env python
+"""Developer workload for profiling the forward FHT (ncu -k regex:k_fwd): N=2048, 4 slices,
+three fbp_fht_forward calls.  Not a test."""
 import json, os, sys, torch
 sys.path.insert(0, os.getcwd())
 import paper_2007_06289_b200 as pkg
