@@ -133,10 +133,12 @@ FBP_API fbp_status fbp_resample_sinogram(const fbp_plan* plan, const float* sino
  * projection with weight w = 1/N (reading R7).
  *   sino: device [batch][4][N][2N];  image: device [batch][N][N].
  * Not required to equal fbp_fht_backproject(fbp_iir_filter(.), 1/N) bitwise.
- * On the fused fast path (fbp_plan_path) the anticausal recursion's carry into
- * each tile of X samples sums the next D tiles only; D is the smallest tile
+ * On the fused fast path (fbp_plan_path) both recursions are truncated to the
+ * same tail bound: the anticausal carry into each tile of X samples sums the
+ * next D tiles only, and a sweep (or sweep segment) starts its causal recursion
+ * from zero state D tiles before the first tile it needs.  D is the smallest tile
  * count whose dropped impulse-response tail is <= 1e-9 of its l1 norm
- * (reading R22).  Otherwise the recursion is exact.
+ * (reading R22).  The general path's recursions are exact.
  */
 FBP_API fbp_status fbp_reconstruct(const fbp_plan* plan, const float* sino, float* image, int batch,
                            void* cuda_stream);
@@ -146,7 +148,9 @@ FBP_API fbp_status fbp_reconstruct(const fbp_plan* plan, const float* sino, floa
  * device (pinned staging, copies overlapped with compute on two internal
  * streams), reconstructs, copies images back.  Synchronous: returns when
  * `image` holds the result.  sino: host [batch][4][N][2N]; image: host [batch][N][N].
- * batch may exceed max_batch (processed in groups).
+ * batch may exceed max_batch (processed in groups).  The plan's host-path staging
+ * is created on first use; concurrent host-path calls on one plan are serialised
+ * (a plan mutex), and the call drains its streams before returning, also on error.
  */
 FBP_API fbp_status fbp_reconstruct_host(const fbp_plan* plan, const float* sino, float* image, int batch);
 

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,7 +27,9 @@ struct fbp_plan {
   float* R = nullptr;       // pass-A output workspace [group][4][NB][H][WR]
   float* lane_mats = nullptr;  // [32][8*8] A^(L*j) for the IIR cross-warp carries
   size_t F_bytes = 0, R_bytes = 0;
-  // host-path staging (allocated lazily by fbp_reconstruct_host)
+  // host-path staging (allocated lazily by fbp_reconstruct_host, under host_mu:
+  // concurrent host-path calls on one plan are serialised)
+  std::mutex host_mu;
   float* d_in[2] = {nullptr, nullptr};
   float* d_out[2] = {nullptr, nullptr};
   float* h_in[2] = {nullptr, nullptr};
@@ -355,14 +358,19 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.nt = sg.W / sg.X;
     sg.P = 0;   // pass B L2 prefetch distance in items: 0 measured best since pair 0 runs 3 CTAs/SM
                 // (0.447 vs 0.453 ms at 1, r01); the TMA double buffer covers the fills
+#if FBP_DEV_MASK
     if (const char* ev = std::getenv("FBP_PREFETCH")) sg.P = std::atoi(ev);
+#endif
     // pass-B x-tile: 64 for NB = 32 (double-buffered TMA fills fit 2 CTAs/SM; measured
     // 5 % faster than 128 single-buffered), 128 otherwise
     sg.XB = (sg.NB == 64) ? 32 : (sg.NB == 32) ? 64 : 128;   // NB = 64 (N = 4096): radix 8+8, single-buffered
+#if FBP_DEV_MASK
+    // developer tuning knobs: compiled in only with -DFBP_DEV_MASK=1
     if (const char* ev = std::getenv("FBP_XB")) sg.XB = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_SWEEP_CTAS")) sg.ctas_a = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_SWEEP_SEG")) sg.nseg = std::atoi(ev);
     if (const char* ev = std::getenv("FBP_DBG")) sg.dbg = std::atoi(ev);
+#endif
     // impulse response of B(z)/A(z) in double; tail bound over lags >= D*X - 2
     const int K = 1 << 16;
     std::vector<double> h(K, 0.0);
@@ -376,9 +384,11 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     int D = 0;
     // R22: dropped tail <= 1e-9 of ||h||_1, ~60x below one fp32 ulp (2^-24) of the
     // carried sums (1e-12 gave bit-identical N = 2048 results with one more tile);
-    // developer override FBP_TAIL (timing studies only)
+    // developer override FBP_TAIL (timing studies only, developer builds only)
     double tail_eps = 1e-9;
+#if FBP_DEV_MASK
     if (const char* ev = std::getenv("FBP_TAIL")) tail_eps = std::atof(ev);
+#endif
     for (int d = 1; d <= 16; ++d) {
       const int lag = std::max(0, d * sg.X - 2);
       if (lag < K && tail[lag] <= tail_eps * tail[0]) {
@@ -586,6 +596,8 @@ fbp_status fbp_reconstruct_host(const fbp_plan* cp, const float* sino, float* im
   if (batch == 0) return FBP_OK;
   if (!sino || !image) return fail(FBP_ERR_PARAM, "NULL data pointer");
   fbp_plan* p = const_cast<fbp_plan*>(cp);
+  // the host path owns plan-level staging and streams: one host call at a time
+  std::lock_guard<std::mutex> lock(p->host_mu);
   DeviceGuard guard(p->device);
   const Geometry& g = p->g;
   const size_t lin_elems = (size_t)4 * g.N * g.W;
@@ -674,10 +686,16 @@ fbp_status fbp_reconstruct_host(const fbp_plan* cp, const float* sino, float* im
     cudaEventRecord(ev_out[slot], p->s_d2h);
     if (!out_pinned) out_group[slot] = gi;
   }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_copy);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_comp);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_d2h);
-  for (int i = 0; i < 2; ++i) flush_out(i);
+  // always drain every stream (also after an error: no copy may still touch the
+  // caller's buffers when this synchronous call returns)
+  {
+    const cudaError_t e1 = cudaStreamSynchronize(p->s_copy);
+    const cudaError_t e2 = cudaStreamSynchronize(p->s_comp);
+    const cudaError_t e3 = cudaStreamSynchronize(p->s_d2h);
+    if (e == cudaSuccess) e = (e1 != cudaSuccess) ? e1 : (e2 != cudaSuccess) ? e2 : e3;
+  }
+  if (e == cudaSuccess)
+    for (int i = 0; i < 2; ++i) flush_out(i);
   for (int i = 0; i < 2; ++i) {
     cudaEventDestroy(ev_in[i]);
     cudaEventDestroy(ev_done[i]);

@@ -4,6 +4,13 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+// Developer builds only (FBP_NVCC_FLAGS=-DFBP_DEV_MASK=1): the FBP_DBG timing skip
+// mask and the FBP_* tuning environment variables.  Product builds
+// read no environment variable.
+#ifndef FBP_DEV_MASK
+#define FBP_DEV_MASK 0
+#endif
+
 namespace fbp {
 
 constexpr int kMaxOrder = 8;       // M, Q <= 8 (fbp.h)
@@ -85,7 +92,7 @@ bool sweep_supported(int N);
 size_t sweep_a_smem(const SweepGeom& g);
 size_t pair_b_smem(const SweepGeom& g, int pair);
 
-// Kernel launchers (kernels.cu).  All asynchronous on `st`; return the launch error.
+// Kernel launchers of the general path (iir.cu, fht.cu).  All asynchronous on `st`; return the launch error.
 // lane_mats: device [32][8*8], lane_mats[j] = A^(L*j).
 cudaError_t launch_iir_rows(const float* in, float* out, long long rows, const Geometry& g,
                             const IirParams& p, const float* lane_mats, cudaStream_t st,

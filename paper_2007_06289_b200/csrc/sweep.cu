@@ -17,7 +17,7 @@
 // into tile j is sum_{i=1..D} (A^X)^(i-1) agg[j+i], agg[t] being the anticausal
 // state at the left edge of tile t produced by the inputs inside tile t; tiles
 // beyond j + D are dropped, and D is chosen by the plan so that the dropped tail
-// of the impulse response is below 1e-12 of its l1 norm (R22).  The
+// of the impulse response is below 1e-9 of its l1 norm (R22).  The
 // look-ahead tile is landed by TMA at the start of a step and reduced at its end;
 // each tile is landed a second time (L2 hit) when it becomes the current tile.
 //
@@ -37,10 +37,8 @@
 #include <algorithm>
 
 // Developer timing mask (env FBP_DBG, tools/dev_timing.py: skip TMA loads / FHT
-// steps / epilogue to attribute time) -- compiled in only with -DFBP_DEV_MASK=1.
-#ifndef FBP_DEV_MASK
-#define FBP_DEV_MASK 0
-#endif
+// steps / epilogue to attribute time) -- compiled in only with -DFBP_DEV_MASK=1
+// (fbp_internal.h).
 
 namespace fbp {
 
@@ -736,8 +734,9 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 // input buffer) and the pair epilogue mirrors, adds, weights and stores:
 //   PAIR 0:  img[ch*NB + r][x0 + i]  = w (B0[r][i] + B1[r][XB-1-i])
 //   PAIR 1:  img[x0 + i][ch*NB + r] += w (B2[r][i] + B3[r][XB-1-i])
-// For PAIR 1 the image rows are staged into shared memory by cp.async while
-// the FHT steps run.  Two CTAs per SM; no cross-item prefetch.
+// For PAIR 1 the image rows are staged into shared memory by TMA while the FHT
+// steps run.  Pair 0 runs 3 CTAs per SM, pair 1 two; the next item's boxes land
+// while this one computes (double buffer).
 // ===========================================================================
 // Pass-B item position (slice, channel, x tile).  Items are visited with the grid
 // stride; the stride is decomposed once and added with mixed-radix carries, so the

@@ -88,8 +88,11 @@ def _check(status: int):
         raise FbpError(status, lib().fbp_last_error().decode())
 
 
-def _stream_ptr(stream) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream, device: int) -> int:
+    """The caller's stream, else the current stream of the plan's device."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    if s.device.index != device:
+        raise ValueError(f"stream is on cuda:{s.device.index}, the plan on cuda:{device}")
     return s.cuda_stream
 
 
@@ -152,32 +155,41 @@ class Plan:
         return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_KINDS)}
 
     # ------------------------------------------------------------- checks
-    def _lin(self, x: torch.Tensor, name: str) -> torch.Tensor:
+    def _dev(self, x: torch.Tensor, name: str):
+        if x.device.index != self.device:
+            raise ValueError(f"{name} is on {x.device}, the plan on cuda:{self.device}")
+
+    def _lin(self, x: torch.Tensor, name: str, batch: int | None = None) -> torch.Tensor:
         N = self.n
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32):
             raise TypeError(f"{name} must be a float32 CUDA tensor")
+        self._dev(x, name)
         if x.dim() == 3:
             x = x.unsqueeze(0)
         if tuple(x.shape[1:]) != (4, N, 2 * N):
             raise ValueError(f"{name} must have shape [B, 4, {N}, {2 * N}], got {tuple(x.shape)}")
         if not x.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
+        if batch is not None and x.shape[0] != batch:
+            raise ValueError(f"{name} has batch {x.shape[0]}, the input {batch}")
         return x
 
     def _img_out(self, out, B):
         N = self.n
         if out is None:
             return torch.empty((B, N, N), device=f"cuda:{self.device}", dtype=torch.float32)
-        if tuple(out.shape) != (B, N, N) or out.dtype != torch.float32 or not out.is_contiguous():
-            raise ValueError("out must be a contiguous float32 [B, N, N] tensor")
+        if (not isinstance(out, torch.Tensor) or not out.is_cuda or tuple(out.shape) != (B, N, N)
+                or out.dtype != torch.float32 or not out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous float32 CUDA [{B}, {N}, {N}] tensor")
+        self._dev(out, "out")
         return out
 
     # ---------------------------------------------------------------- ops
     def iir_filter(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):
         x = self._lin(sino, "sino")
-        out = torch.empty_like(x) if out is None else self._lin(out, "out")
+        out = torch.empty_like(x) if out is None else self._lin(out, "out", x.shape[0])
         _check(lib().fbp_iir_filter(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
-                                    _stream_ptr(stream)))
+                                    _stream_ptr(stream, self.device)))
         return out
 
     def backproject(self, lin: torch.Tensor, scale: float = 1.0, out: torch.Tensor | None = None,
@@ -185,7 +197,7 @@ class Plan:
         x = self._lin(lin, "lin")
         out = self._img_out(out, x.shape[0])
         _check(lib().fbp_fht_backproject(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
-                                         float(scale), _stream_ptr(stream)))
+                                         float(scale), _stream_ptr(stream, self.device)))
         return out
 
     def forward(self, image: torch.Tensor, out: torch.Tensor | None = None, stream=None):
@@ -197,12 +209,14 @@ class Plan:
             image = image.unsqueeze(0)
         if tuple(image.shape[1:]) != (N, N) or not image.is_contiguous():
             raise ValueError(f"image must be a contiguous [B, {N}, {N}] tensor, got {tuple(image.shape)}")
+        self._dev(image, "image")
         B = image.shape[0]
         if out is None:
             out = torch.empty((B, 4, N, 2 * N), device=image.device, dtype=torch.float32)
         else:
-            out = self._lin(out, "out")
-        _check(lib().fbp_fht_forward(self._h, image.data_ptr(), out.data_ptr(), B, _stream_ptr(stream)))
+            out = self._lin(out, "out", B)
+        _check(lib().fbp_fht_forward(self._h, image.data_ptr(), out.data_ptr(), B,
+                                     _stream_ptr(stream, self.device)))
         return out
 
     def resample(self, sino: torch.Tensor, dr: float = 1.0, out: torch.Tensor | None = None, stream=None):
@@ -214,39 +228,53 @@ class Plan:
             sino = sino.unsqueeze(0)
         if sino.dim() != 3 or not sino.is_contiguous():
             raise ValueError(f"sino must be a contiguous [B, n_angles, n_bins] tensor, got {tuple(sino.shape)}")
+        self._dev(sino, "sino")
         B, na, nb = sino.shape
         if out is None:
             out = torch.empty((B, 4, N, 2 * N), device=sino.device, dtype=torch.float32)
         else:
-            out = self._lin(out, "out")
+            out = self._lin(out, "out", B)
         _check(lib().fbp_resample_sinogram(self._h, sino.data_ptr(), na, nb, float(dr), out.data_ptr(), B,
-                                           _stream_ptr(stream)))
+                                           _stream_ptr(stream, self.device)))
         return out
 
     def reconstruct(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None):
         x = self._lin(sino, "sino")
         out = self._img_out(out, x.shape[0])
         _check(lib().fbp_reconstruct(self._h, x.data_ptr(), out.data_ptr(), x.shape[0],
-                                     _stream_ptr(stream)))
+                                     _stream_ptr(stream, self.device)))
         return out
 
     def reconstruct_host(self, sino, out=None):
-        """Host buffers in, host buffers out (numpy or CPU torch, float32, contiguous)."""
+        """Host buffers in, host buffers out (numpy or CPU torch, float32, contiguous).
+
+        Synchronous.  `out` (if given) must be a contiguous float32 host buffer of
+        shape [B, N, N] of the same kind as `sino`: the library writes B*N*N floats
+        into it.  Not thread-safe per plan: one host thread per plan."""
         N = self.n
+        want = (4, N, 2 * N)
         if isinstance(sino, torch.Tensor):
             if sino.is_cuda or sino.dtype != torch.float32 or not sino.is_contiguous():
                 raise TypeError("sino must be a contiguous float32 CPU tensor")
+            if sino.dim() != 4 or tuple(sino.shape[1:]) != want:
+                raise ValueError(f"sino must have shape [B, 4, {N}, {2 * N}], got {tuple(sino.shape)}")
             B = sino.shape[0]
             if out is None:
                 out = torch.empty((B, N, N), dtype=torch.float32, pin_memory=sino.is_pinned())
+            elif (not isinstance(out, torch.Tensor) or out.is_cuda or out.dtype != torch.float32
+                  or not out.is_contiguous() or tuple(out.shape) != (B, N, N)):
+                raise ValueError(f"out must be a contiguous float32 CPU tensor of shape [{B}, {N}, {N}]")
             ptr_in, ptr_out = sino.data_ptr(), out.data_ptr()
         else:
             sino = np.ascontiguousarray(sino, dtype=np.float32)
+            if sino.ndim != 4 or tuple(sino.shape[1:]) != want:
+                raise ValueError(f"sino must have shape [B, 4, {N}, {2 * N}], got {tuple(sino.shape)}")
             B = sino.shape[0]
             if out is None:
                 out = np.empty((B, N, N), dtype=np.float32)
+            elif (not isinstance(out, np.ndarray) or out.dtype != np.float32
+                  or not out.flags["C_CONTIGUOUS"] or not out.flags["WRITEABLE"] or out.shape != (B, N, N)):
+                raise ValueError(f"out must be a writeable C-contiguous float32 array of shape [{B}, {N}, {N}]")
             ptr_in, ptr_out = sino.ctypes.data, out.ctypes.data
-        if tuple(sino.shape[1:]) != (4, N, 2 * N):
-            raise ValueError("sino must have shape [B, 4, N, 2N]")
         _check(lib().fbp_reconstruct_host(self._h, ptr_in, ptr_out, B))
         return out

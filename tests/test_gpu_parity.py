@@ -192,6 +192,80 @@ def test_reconstruct_full_size(fbp, cfg):
     assert np.max(np.abs(got - ref)) <= TOL * np.max(np.abs(ref0))
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_fast_path_spec_coefficients_full_image(fbp, cfg):
+    """The fast path with the SPEC plain-MSE coefficients (beta = sum b != 0, so the
+    sweep's BETA feedforward term runs): whole image vs the full oracle.
+    (Eq.12-13; R16 difference form with beta.)"""
+    N = P.CONFIGS[cfg]["N"]
+    b, a = coeffs(N, "spec")
+    assert abs(sum(b)) > 1e-6
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    assert plan.path()["fast"]
+    S = P.make_slice(cfg, 0, device="cuda").unsqueeze(0)
+    img = plan.reconstruct(S).cpu().numpy()[0]
+    ref = O.reconstruct(S[0].cpu().double().numpy(), b, a)
+    assert rel_err(img, ref) < TOL
+
+
+def test_fast_path_spec_coefficients_4096_sampled(fbp):
+    """N = 4096 (config-5 size) with the spec coefficients: sampled pixels, each summed
+    by the oracle along its dyadic lines after the oracle IIR of every row; scale = the
+    slice's peak (GPU image peak; within 1e-4 of the oracle's when parity holds)."""
+    N = 4096
+    b, a = coeffs(N, "spec")
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    assert plan.path()["fast"]
+    S = P.make_slice(5, 0, device="cuda").unsqueeze(0)
+    img = plan.reconstruct(S).cpu().numpy()[0]
+    got, ref = _sampled_check(img, S[0].cpu().numpy(), b, a, n_pts=16, seed=5)
+    assert np.max(np.abs(got - ref)) <= TOL * float(np.abs(img).max())
+
+
+@pytest.mark.parametrize("N,cfg,B,variant", [(2048, 3, 16, "dc0"), (2048, 3, 16, "spec"), (4096, 5, 8, "dc0")])
+def test_bench_launch_configuration(fbp, N, cfg, B, variant):
+    """bench.py's own launch: N = 2048 with 16 slices per call (the sweep runs one
+    segment per sweep, nseg = 1) and N = 4096 with 8.  Slice 0: whole image vs the full
+    oracle (N = 2048) or sampled pixels (N = 4096); every other slice: sampled pixels
+    (oracle IIR of every row + direct dyadic-line sums), scale = that slice's peak."""
+    b, a = coeffs(N, variant)
+    plan = fbp.Plan(N, b, a, max_batch=B)
+    assert plan.path()["fast"]
+    S = P.make_batch(cfg, B, device="cuda")
+    img = plan.reconstruct(S).cpu().numpy()
+    if N <= 2048:
+        ref0 = O.reconstruct(S[0].cpu().double().numpy(), b, a)
+        assert rel_err(img[0], ref0) < TOL
+        first = 1
+    else:
+        first = 0
+    for i in range(first, B):
+        if N > 2048 and i not in (0, B // 2, B - 1):
+            continue
+        got, ref = _sampled_check(img[i], S[i].cpu().numpy(), b, a, n_pts=6, seed=100 + i)
+        assert np.max(np.abs(got - ref)) <= TOL * float(np.abs(img[i]).max()), i
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_path_multi_stage(fbp, pinned):
+    """fbp_reconstruct_host over 9 slices: 3 pipeline stages of at most 4 slices
+    (double-buffered slots, ev_done reuse, unpinned flush) bit-equal to the device path."""
+    N = 512
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=9)
+    S = P.make_batch(2, 9, N=N)
+    dev = plan.reconstruct(S.cuda()).cpu()
+    if pinned:
+        h = plan.reconstruct_host(S.pin_memory())
+        assert torch.equal(h, dev)
+    else:
+        h = plan.reconstruct_host(S.numpy())
+        assert np.array_equal(h, dev.numpy())
+    # a second call through the same (now allocated) staging
+    h2 = plan.reconstruct_host(S.numpy())
+    assert np.array_equal(h2, dev.numpy())
+
+
 def test_reconstruct_full_size_config5(fbp):
     N = 4096
     b, a = coeffs(N)
