@@ -11,14 +11,14 @@ Timing: W warm-up steps, barrier + synchronize, CUDA events on the launching
 stream around exactly K steps, max over ranks.  Inputs (B x 128 MiB) exceed the
 126 MB L2, so no flush is needed between steps.
 
-Rank 0 prints ONE JSON line.  See DESIGN.md §8 for every field.
+Rank 0 prints ONE JSON line.  See DESIGN.md §7-8 for every field.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -44,6 +44,66 @@ def measured_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured", float(d.get("sm_max_mhz", 1965.0))
     return 6650.0, "fallback", 1965.0
+
+
+# ------------------------------------------------------------- rank logic
+# (backend-agnostic; tests/test_bench_ranks.py drives it with gloo on CPU)
+def rank_env():
+    """(world, rank, local_rank) from the torchrun environment (1, 0, 0 without)."""
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def slice_ids(rank: int, per_rank: int) -> list:
+    """Distinct seeded slices per rank: rank r owns slices r*B .. r*B + B - 1."""
+    return [rank * per_rank + i for i in range(per_rank)]
+
+
+def time_steps(step, steps: int, barrier, sync, timer) -> float:
+    """Barrier + sync, then exactly `steps` calls of step() between timer marks,
+    sync + barrier.  timer() -> (start(), stop() -> ms)."""
+    barrier()
+    sync()
+    start, stop = timer()
+    start()
+    for _ in range(steps):
+        step()
+    ms = stop()
+    sync()
+    barrier()
+    return ms
+
+
+def max_over_ranks(values, world: int, device="cpu"):
+    """Element-wise max of per-rank timings (all_reduce MAX; identity at world 1)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.cpu()]
+
+
+def aggregate(world: int, per_rank: int, steps: int, max_ms: float) -> float:
+    """Whole-job throughput: slices of all ranks / slowest rank's time."""
+    return world * per_rank * steps / (max_ms / 1e3)
+
+
+def cuda_timer(stream):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+
+    def make():
+        def start():
+            e0.record(stream)
+
+        def stop():
+            e1.record(stream)
+            e1.synchronize()
+            return e0.elapsed_time(e1)
+        return start, stop
+    return make
 
 
 # ------------------------------------------------------------------ clocks
@@ -103,8 +163,14 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- roofline
-def kernel_algorithmic_bytes(kind: str, N: int, NB: int, H: int, path: dict | None = None) -> float:
-    """Algorithmic HBM bytes per SLICE of each kernel."""
+def alg_bytes_per_slice(N: int) -> float:
+    """read the 4 x N x 2N fp32 linogram, write the N x N fp32 image."""
+    return 36.0 * N * N
+
+
+def kernel_design_bytes(kind: str, N: int, NB: int, H: int, path: dict | None = None) -> float:
+    """Bytes per SLICE each kernel's own contract must move, including
+    the two-pass FHT's intermediate R; reported beside, not instead of, §8(d)."""
     W = 2 * N
     lin = 4.0 * N * W * 4                                  # 32 N^2 B
     # compact pass-A output: per family sum_b H rows of (N + b) floats
@@ -126,65 +192,136 @@ def kernel_algorithmic_bytes(kind: str, N: int, NB: int, H: int, path: dict | No
 
 
 def ncu_traffic(kind: str):
-    """DRAM bytes per launch of `kind` from the committed ncu --set full summary."""
+    """ncu DRAM bytes per slice of `kind` from the committed bench-batch capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     d = json.load(open(p))
     v = d.get(kind)
-    return v.get("dram_bytes_per_slice") if isinstance(v, dict) else None
+    if not isinstance(v, dict):
+        return None, None
+    return v.get("dram_bytes_per_slice"), v.get("source")
+
+
+# ------------------------------------------------------- CPU oracle pool
+_POOL_DATA = {}
+
+
+def _pool_reconstruct(i):
+    """Worker: the oracle on slice i % len(slices) (fork-inherited, untimed setup)."""
+    from oracle import fbp_oracle as O
+    S, b, a = _POOL_DATA["slices"][i % len(_POOL_DATA["slices"])], _POOL_DATA["b"], _POOL_DATA["a"]
+    t0 = time.perf_counter()
+    if _POOL_DATA.get("family") is None:
+        O.reconstruct(S, b, a)
+    else:
+        import numpy as np
+        f = (i + _POOL_DATA["family"]) % 4
+        F = np.zeros_like(S)
+        F[f] = O.iir_symmetric(S[f], b, a)
+        O.combine(O.fht_backproject(F), 1.0 / S.shape[1])
+    return time.perf_counter() - t0, time.time()
+
+
+def host_cores():
+    """(threads usable by this process, os.cpu_count(), CPU model)."""
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return usable, os.cpu_count(), model
+
+
+def pool_workers(per_worker_gb: float) -> int:
+    usable, _, _ = host_cores()
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE") / 2**30
+        cap = max(1, int(0.6 * avail / per_worker_gb))
+    except (ValueError, OSError):
+        cap = usable
+    return max(1, min(usable, cap))
+
+
+class OraclePool:
+    """The oracle as it stands, one single-threaded NumPy process per host core
+    (fork start method: the seeded slices are inherited, not pickled)."""
+
+    def __init__(self, slices, b, a, family=None, per_worker_gb=1.6):
+        import multiprocessing as mp
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        _POOL_DATA.update(slices=slices, b=b, a=a, family=family)
+        self.workers = pool_workers(per_worker_gb)
+        self.pool = mp.get_context("fork").Pool(self.workers)
+
+    def step(self, k: int = 0):
+        """One round: every worker runs one task; returns the round's wall seconds."""
+        t0 = time.time()
+        res = self.pool.map(_pool_reconstruct, [k * self.workers + i for i in range(self.workers)],
+                            chunksize=1)
+        return max(r[1] for r in res) - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(slices_np, b, a):
+    """Oracle throughput on a bounded sample of the same workload (rank 0, N=1):
+    one full config-3 slice per host core, all in parallel."""
+    usable, total, model = host_cores()
+    pool = OraclePool(slices_np, b, a)
+    dt = pool.step()
+    w = pool.workers
+    pool.close()
+    return {"value": w / dt, "unit": UNIT, "cores": w, "kind": "oracle",
+            "sample": f"{w} full config-3 slices (N=2048), one per process, NumPy fp64 oracle.reconstruct",
+            "seconds": dt, "host_cpu_count": total, "affinity_cores": usable, "cpu_model": model}
 
 
 # ---------------------------------------------------------------- arms
 def run_reference(args):
-    """The oracle as it stands, on host cores (bench --impl reference)."""
-    import numpy as np
-    import torch
-    import phantoms
-    from oracle import fbp_oracle as O
-    rank = int(os.environ.get("RANK", "0"))
+    """The oracle as it stands, on the box's host cores (bench --impl reference)."""
+    world, rank, _ = rank_env()
     if rank != 0:
         return
+    import phantoms
     N = N_HEADLINE
     b, a = load_coeffs(N)
-    # one step = the oracle on one line family of one slice (IIR on its N rows,
-    # FHT back projection, its share of Eq.22): a bounded quarter-slice sample.
-    S = phantoms.make_slice(CFG, 0).double().numpy()
-    def step(f):
-        F = O.iir_symmetric(S[f], b, a)
-        Ff = np.zeros((4, N, 2 * N))
-        Ff[f] = F
-        return O.combine(O.fht_backproject(Ff), 1.0 / N)
-    for i in range(args.warmup):
-        step(i % 4)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(i % 4)
-    dt = time.perf_counter() - t0
-    value = 0.25 * args.steps / dt
+    slices = [phantoms.make_slice(CFG, i).double().numpy() for i in range(2)]
+    # one step = one line family of one slice per host core (IIR on its N rows,
+    # FHT back projection, its share of Eq.22), all cores in parallel
+    pool = OraclePool(slices, b, a, family=0)
+    for k in range(args.warmup):
+        pool.step(k)
+    dt = 0.0
+    for k in range(args.steps):
+        dt += pool.step(args.warmup + k)
+    w = pool.workers
+    pool.close()
+    usable, total, model = host_cores()
+    value = 0.25 * w * args.steps / dt
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config3: N=2048 slice, 4x2048x4096 linogram, 50-ellipse phantom",
-                       "N": N, "step": "one line family of one slice (0.25 slice)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} quarter-slices (one family each) of config-3 slice 0"},
+                       "N": N, "step": f"one line family of one slice on each of {w} host processes "
+                                       f"({0.25 * w:g} slices)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": w, "kind": "oracle",
+                             "sample": f"{args.steps} steps x {w} quarter-slices (one family each) "
+                                       "of config-3 slices 0-1", "host_cpu_count": total,
+                             "affinity_cores": usable, "cpu_model": model},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def cpu_baseline(N, b, a, budget_s=25.0):
-    """Oracle on a bounded sample of the same workload, rank 0 at N=1."""
-    import phantoms
-    from oracle import fbp_oracle as O
-    S = phantoms.make_slice(CFG, 0).double().numpy()
-    t0 = time.perf_counter()
-    O.reconstruct(S, b, a)
-    dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "1 full config-3 slice (N=2048) through oracle.reconstruct, NumPy fp64, 1 thread",
-            "seconds": dt}
 
 
 def run_fbp(args):
@@ -192,10 +329,9 @@ def run_fbp(args):
     import torch.distributed as dist
     import phantoms
     import paper_2007_06289_b200 as pkg
+    from paper_2007_06289_b200 import dist as fdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = rank_env()
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -204,14 +340,14 @@ def run_fbp(args):
         local = 0
     dev = torch.device(f"cuda:{local}")
     N = args.n
-    b, a = load_coeffs(N)
+    b, a = load_coeffs(N, args.coeffs)
     B = args.batch
     plan = pkg.Plan(N, b, a, max_batch=B, device=local)
     info = plan.info()
-    # distinct seeded slices per rank: slice index rank*B + i
+    # distinct seeded slices per rank
     S = torch.empty((B, 4, N, 2 * N), device=dev, dtype=torch.float32)
-    for i in range(B):
-        S[i] = phantoms.make_slice(CFG, rank * B + i, device=dev, N=N)
+    for i, sid in enumerate(slice_ids(rank, B)):
+        S[i] = phantoms.make_slice(CFG, sid, device=dev, N=N)
     img = torch.empty((B, N, N), device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream(dev)
 
@@ -219,44 +355,67 @@ def run_fbp(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(max(args.warmup, 0)):
+    def sync():
+        torch.cuda.synchronize(dev)
+
+    timer = cuda_timer(stream)
+    launches = [0]
+
+    def step():
         plan.reconstruct(S, out=img, stream=stream)
-    torch.cuda.synchronize(dev)
+
+    def step_counted():
+        step()
+        launches[0] += plan.launch_count()
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    sync()
 
     sampler = ClockSampler(local)
     sampler.start()
-    barrier()
-    torch.cuda.synchronize(dev)
     plan.profile(True)
-    launches = 0
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        plan.reconstruct(S, out=img, stream=stream)
-        launches += plan.launch_count()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
-    ms = e0.elapsed_time(e1)
+    ms = time_steps(step_counted, args.steps, barrier, sync, timer)
     ktimes = plan.kernel_times()
     plan.profile(False)
     # a clean (event-free) timing of the same K steps, for the headline value
-    torch.cuda.synchronize(dev)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        plan.reconstruct(S, out=img, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
-    ms_clean = e0.elapsed_time(e1)
+    ms_clean = time_steps(step, args.steps, barrier, sync, timer)
     clocks = sampler.stop()
+    ms_clean, ms = max_over_ranks([ms_clean, ms], world, dev)
 
-    t = torch.tensor([ms_clean, ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_clean, ms = float(t[0]), float(t[1])
+    # ---- the SPEC plain-MSE coefficient set (beta != 0 sweep variant), same workload ----
+    variants = {}
+    if not args.no_variants and args.coeffs != "spec":
+        bs, as_ = load_coeffs(N, "spec")
+        plan_s = pkg.Plan(N, bs, as_, max_batch=B, device=local)
+        for _ in range(3):
+            plan_s.reconstruct(S, out=img, stream=stream)
+        ks = max(3, min(args.steps, 20))
+        plan_s.profile(True)
+        ms_s = time_steps(lambda: plan_s.reconstruct(S, out=img, stream=stream), ks, barrier, sync, timer)
+        kt_s = plan_s.kernel_times()
+        plan_s.profile(False)
+        ms_s = max_over_ranks([ms_s], world, dev)[0]
+        variants["spec"] = {"value": aggregate(world, B, ks, ms_s), "unit": UNIT, "steps": ks,
+                            "ms_per_step": ms_s / ks, "coeffs": "spec M=Q=3 (plain MSE fit, beta != 0)",
+                            "schedule": plan_s.path(),
+                            "kernel_ms_per_step": {k: v[0] / ks for k, v in kt_s.items() if v[1] > 0}}
+        plan_s.close()
+        del plan_s
+
+    # ---- multi-GPU: gather every rank's images to rank 0 (NCCL), timed separately ----
+    gather = None
+    if world > 1 and not args.no_gather:
+        n_total = world * B
+        for _ in range(2):
+            fdist.gather_volume(img, n_total, N, world, rank, dev)
+        ms_g = time_steps(lambda: fdist.gather_volume(img, n_total, N, world, rank, dev), 3, barrier, sync,
+                          timer)
+        ms_g = max_over_ranks([ms_g], world, dev)[0] / 3
+        gather = {"ms": ms_g, "bytes_to_rank0": (world - 1) * B * N * N * 4,
+                  "GB_per_s_into_rank0": (world - 1) * B * N * N * 4 / (ms_g / 1e3) / 1e9,
+                  "how": "torch.distributed.gather (NCCL) of [B, N, N] fp32 per rank to rank 0, "
+                         "not in the headline timed region"}
 
     # ---- NEXT-1: forward FHT (fbp_fht_forward, Eq.17) of this step's images ----
     fwd = None
@@ -265,24 +424,13 @@ def run_fbp(args):
         for _ in range(3):
             plan.forward(img, out=lin_f, stream=stream)
         kf = max(1, min(args.steps, 20))
-        torch.cuda.synchronize(dev)
-        barrier()
         plan.profile(True)
-        e0.record(stream)
-        for _ in range(kf):
-            plan.forward(img, out=lin_f, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        ms_f = e0.elapsed_time(e1)
+        ms_f = time_steps(lambda: plan.forward(img, out=lin_f, stream=stream), kf, barrier, sync, timer)
         kt_f = plan.kernel_times()
         plan.profile(False)
-        tf = torch.tensor([ms_f], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tf, op=dist.ReduceOp.MAX)
-        ms_f = float(tf[0])
+        ms_f = max_over_ranks([ms_f], world, dev)[0]
         alg_f = 36.0 * N * N                   # image read (4 N^2 B) + linogram write (32 N^2 B)
-        fwd = {"value": world * B * kf / (ms_f / 1e3), "unit": UNIT, "steps": kf, "ms_per_step": ms_f / kf,
+        fwd = {"value": aggregate(world, B, kf, ms_f), "unit": UNIT, "steps": kf, "ms_per_step": ms_f / kf,
                "input": "this step's reconstructed images", "gpu_launches_per_step": plan.launch_count(),
                "kernel_ms_per_step": {k: v[0] / kf for k, v in kt_f.items() if v[1] > 0},
                "roofline": {"bound": "hbm", "alg_bytes_per_slice": alg_f, "unit": "GB/s per GPU",
@@ -303,21 +451,11 @@ def run_fbp(args):
         for _ in range(3):
             plan.resample(sino, dr=dr, out=lin_r, stream=stream)
         kr = max(1, min(args.steps, 20))
-        torch.cuda.synchronize(dev)
-        barrier()
-        e0.record(stream)
-        for _ in range(kr):
-            plan.resample(sino, dr=dr, out=lin_r, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        ms_r = e0.elapsed_time(e1)
-        tr = torch.tensor([ms_r], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tr, op=dist.ReduceOp.MAX)
-        ms_r = float(tr[0])
+        ms_r = time_steps(lambda: plan.resample(sino, dr=dr, out=lin_r, stream=stream), kr, barrier, sync,
+                          timer)
+        ms_r = max_over_ranks([ms_r], world, dev)[0]
         alg_r = 4.0 * na * nb + 32.0 * N * N        # sinogram read + linogram write
-        rsm = {"value": world * B * kr / (ms_r / 1e3), "unit": UNIT, "steps": kr, "ms_per_step": ms_r / kr,
+        rsm = {"value": aggregate(world, B, kr, ms_r), "unit": UNIT, "steps": kr, "ms_per_step": ms_r / kr,
                "input": f"analytic 50-ellipse sinogram, {na} angles x {nb} bins, dr={dr}",
                "gpu_launches_per_step": plan.launch_count(),
                "roofline": {"bound": "hbm", "alg_bytes_per_slice": alg_r, "unit": "GB/s per GPU",
@@ -337,58 +475,67 @@ def run_fbp(args):
         for _ in range(reps):
             plan.reconstruct_host(host_in, out=host_out)
         dt = time.perf_counter() - t0
-        te = torch.tensor([dt], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        dt = float(te[0])
+        dt = max_over_ranks([dt], world, dev)[0]
         e2e = {"value": world * Be * reps / dt, "unit": UNIT,
                "h2d_bytes_per_step": Be * 4 * N * 2 * N * 4, "d2h_bytes_per_step": Be * N * N * 4,
                "slices_per_step": Be, "path": "fbp_reconstruct_host (pinned host buffers)"}
 
     if rank == 0:
         peak, peak_kind, _ = measured_peaks()
-        total = world * B * args.steps
-        value = total / (ms_clean / 1e3)
-        # dominant kernel
+        value = aggregate(world, B, args.steps, ms_clean)
+        # dominant kernel: SURVEY §8(d) algorithmic bytes (36 N^2 per slice) x the slices
+        # one launch processes / its mean launch time (CUDA events on the launching stream)
         kinds = {k: v for k, v in ktimes.items() if v[1] > 0}
         dom = max(kinds, key=lambda k: kinds[k][0])
         dom_ms, dom_n = kinds[dom]
-        slices_per_launch = (B * args.steps) / dom_n if dom != "fht_pass_b" else (B * args.steps) / (dom_n / 2)
-        alg = kernel_algorithmic_bytes(dom, N, 1 << info["m"], 1 << info["k1"], plan.path())
+        per_step = dom_n / args.steps                     # launches of `dom` per step
+        # pass B runs one launch per Eq.22 family pair, each over the same slices
+        slices_per_launch = B / max(1.0, per_step / (2 if dom == "fht_pass_b" else 1))
+        alg_launch = alg_bytes_per_slice(N) * slices_per_launch
+        avg_launch_ms = dom_ms / dom_n
+        achieved = alg_launch / (avg_launch_ms / 1e3) / 1e9
+        design = kernel_design_bytes(dom, N, 1 << info["m"], 1 << info["k1"], plan.path())
         if dom == "fht_pass_b":
-            alg = alg / 2                     # one launch = one family pair
-        per_launch_bytes = alg * slices_per_launch
-        achieved = per_launch_bytes / (dom_ms / dom_n / 1e3) / 1e9
-        trf = ncu_traffic(dom)
+            design /= 2                                   # one launch = one family pair
+        design_launch = design * slices_per_launch
+        trf, trf_src = ncu_traffic(dom)
         if trf is not None:
-            trf = trf * slices_per_launch               # per launch, like `achieved`
+            trf = trf * slices_per_launch / (2 if dom == "fht_pass_b" else 1)
         shares = {k: round(v[0] / max(ms, 1e-9), 4) for k, v in ktimes.items()}
-        path_bytes = 36.0 * N * N * total
+        path_bytes = alg_bytes_per_slice(N) * world * B * args.steps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_clean / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config3: N=2048 slices, 4x2048x4096 fp32 linogram each, "
                                    "seeded 50-ellipse phantoms (analytic line integrals)",
-                       "N": N, "slices_per_gpu_per_step": B, "coeffs": "dc0 M=Q=3",
+                       "N": N, "slices_per_gpu_per_step": B, "coeffs": f"{args.coeffs} M=Q=3",
                        "l2": f"inputs {B * 4 * N * 2 * N * 4 / 2**30:.1f} GiB/step per GPU > 126 MB L2 (no flush needed)",
                        "level_split": f"k1={info['k1']} m={info['m']}",
                        "schedule": plan.path(),
                        "parallelism": f"slices sharded over {world} GPU(s), no collective"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": trf, "alg_bytes_per_launch": per_launch_bytes,
-                         "avg_launch_ms": dom_ms / dom_n},
-            "path_roofline": {"alg_bytes_per_slice": 36.0 * N * N,
+                         "alg_bytes_per_launch": alg_launch,
+                         "alg_bytes": "SURVEY 8(d): 36 N^2 B per slice x slices per launch",
+                         "avg_launch_ms": avg_launch_ms, "launches_per_step": per_step,
+                         "traffic": trf, "traffic_source": trf_src,
+                         "design_bytes_per_launch": design_launch,
+                         "design_frac": design_launch / (avg_launch_ms / 1e3) / 1e9 / peak},
+            "path_roofline": {"alg_bytes_per_slice": alg_bytes_per_slice(N),
                               "achieved": path_bytes / (ms_clean / 1e3) / 1e9 / world,
                               "frac": path_bytes / (ms_clean / 1e3) / 1e9 / world / peak,
                               "unit": "GB/s per GPU"},
             "kernel_share": shares,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
-            "gpu_launches": launches,
+            "gpu_launches": launches[0],
             "clocks": clocks,
             "e2e": e2e,
         }
+        if variants:
+            line["variants"] = variants
+        if gather:
+            line["gather"] = gather
         nxt = {}
         for key, item in (("fht_forward", fwd), ("resample", rsm)):
             if item is not None:
@@ -398,7 +545,10 @@ def run_fbp(args):
         if nxt:
             line["next"] = nxt
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(N, b, a)
+            del S, img
+            torch.cuda.empty_cache()
+            slices_np = [phantoms.make_slice(CFG, i).double().numpy() for i in range(2)]
+            line["cpu_baseline"] = cpu_baseline(slices_np, b, a)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -412,11 +562,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=16, help="slices per GPU per step")
     ap.add_argument("--n", type=int, default=N_HEADLINE)
+    ap.add_argument("--coeffs", default="dc0", choices=["dc0", "spec"])
     ap.add_argument("--impl", default="fbp", choices=["fbp", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-batch", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the spec-coefficient line")
+    ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-forward", action="store_true", help="skip the NEXT-1/NEXT-2 line items (forward FHT, resampling)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -3,8 +3,8 @@ collective on the data path; NCCL only to gather results.
 
 Slices of a volume are independent (each is its own linogram -> image), so rank r
 of G owns the contiguous slice range ``shard(n_slices, G, r)`` and runs its own
-``Plan`` on its own GPU.  ``gather_volume`` collects the per-rank images on rank 0
-(``torch.distributed`` gather: NCCL over NVLink on GPUs, gloo on CPU tensors).
+``Plan`` on its own GPU.  ``gather_volume`` collects the per-rank images on rank 0 only
+(``torch.distributed.gather``: NCCL over NVLink on GPUs, gloo on CPU tensors).
 """
 from __future__ import annotations
 
@@ -55,14 +55,10 @@ def gather_volume(local: torch.Tensor | None, n_slices: int, N: int, world: int,
         buf[: local.shape[0]].copy_(local)
     if world == 1:
         return buf[:n_slices].clone()
+    # gather to rank 0 only (NCCL: grouped point-to-point sends into rank 0 over
+    # NVLink; gloo on CPU tensors); the other ranks receive nothing
     parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
-    if dist.get_backend() == "nccl":
-        # NCCL gather is point-to-point under the hood; all_gather keeps it one call
-        allp = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(allp, buf)
-        parts = allp if rank == 0 else None
-    else:
-        dist.gather(buf, gather_list=parts, dst=0)
+    dist.gather(buf, gather_list=parts, dst=0)
     if rank != 0:
         return None
     vol = torch.empty((n_slices, N, N), dtype=torch.float32, device=device)
