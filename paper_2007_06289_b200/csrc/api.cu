@@ -353,8 +353,8 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     sg.W = 2 * n;
     sg.NB = p->g.NB;
     sg.H = p->g.H;
-    sg.WR = p->g.WR;
     sg.X = 4096 / sg.H;
+    sg.WR = p->g.WR;
     sg.nt = sg.W / sg.X;
     sg.P = 0;   // pass B L2 prefetch distance in items: 0 measured best since pair 0 runs 3 CTAs/SM
                 // (0.447 vs 0.453 ms at 1, r01); the TMA double buffer covers the fills
@@ -389,7 +389,7 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
 #if FBP_DEV_MASK
     if (const char* ev = std::getenv("FBP_TAIL")) tail_eps = std::atof(ev);
 #endif
-    for (int d = 1; d <= 16; ++d) {
+    for (int d = 1; d <= 15; ++d) {   // (D+1) x 32 tensor-memory columns <= 512
       const int lag = std::max(0, d * sg.X - 2);
       if (lag < K && tail[lag] <= tail_eps * tail[0]) {
         D = d;
@@ -419,6 +419,16 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
       put(si.M2, 64);
       put(si.MX, sg.X);
       put(si.M16, 16);
+      for (int i = 0; i < 32; ++i) {   // anticausal homogeneous response table (sweep back step)
+        matpow(3, A3, 32 - i, Pm);
+        for (int m2 = 0; m2 < 3; ++m2) {
+          if (i & 1) si.GA[i >> 1][m2].y = (float)Pm[(size_t)m2];
+          else si.GA[i >> 1][m2].x = (float)Pm[(size_t)m2];
+        }
+      }
+      int cols = 32;
+      while (cols < 32 * (D + 1)) cols *= 2;
+      sg.tmem_cols = cols;
       p->fast = true;
     }
   }
@@ -427,7 +437,9 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
   const Geometry& g = p->g;
   const size_t f_slice = p->fast ? 0 : (size_t)4 * g.N * g.W * sizeof(float);
   // R also serves fbp_fht_forward's pass-A output (fwd_workspace_floats per slice)
-  const size_t r_slice = std::max((size_t)4 * g.NB * g.H * g.WR, fwd_workspace_floats(g)) * sizeof(float);
+  const size_t r_rows = (size_t)4 * g.NB * g.H;
+  const size_t r_slice = std::max(r_rows * (p->fast ? (size_t)p->sg.WR : (size_t)g.WR), fwd_workspace_floats(g)) *
+                         sizeof(float);
   // fast path: the whole max_batch in one group up to 8 GiB of R (a small trailing
   // group would leave most of the 444 sweep CTA slots idle); general path: 256 MiB
   const size_t budget = p->fast ? ((size_t)8 << 30) : ((size_t)256 << 20);

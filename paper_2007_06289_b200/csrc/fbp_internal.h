@@ -63,6 +63,10 @@ struct SweepIir {
   float2 M2[9];               // A^64
   float2 MX[9];               // A^X   (one tile)
   float2 M16[9];              // A^16
+  // GA[p][m] = (G^(2p), G^(2p+1)) with G^(i) = (A^(32-i))_{0m}: the anticausal
+  // homogeneous response at sample i of a 32-sample chunk to the state at the
+  // chunk's right edge (adjacent samples packed for FFMA2)
+  float2 GA[16][3];
 };
 
 struct SweepGeom {
@@ -74,10 +78,11 @@ struct SweepGeom {
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
   int nseg;   // segments per sweep (0: automatic, fill the CTA slots); env FBP_SWEEP_SEG
+  int tmem_cols;  // tensor-memory columns per sweep CTA: (D+1) x 32 rounded to a power of two
   int dbg;    // developer timing mask, env FBP_DBG, honoured only in -DFBP_DEV_MASK=1 builds
               // (results invalid when nonzero): pass B bit 0
               // skips the FHT steps, bit 1 the epilogue, bit 2 the fills; sweep bit 3
-              // skips every TMA load
+              // skips every TMA load, bit 4 the R stores
 };
 
 // Pass A sweep over `slices` x families [f0, f0+nf) (input family fi of slice s at

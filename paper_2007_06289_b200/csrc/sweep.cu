@@ -17,9 +17,14 @@
 // into tile j is sum_{i=1..D} (A^X)^(i-1) agg[j+i], agg[t] being the anticausal
 // state at the left edge of tile t produced by the inputs inside tile t; tiles
 // beyond j + D are dropped, and D is chosen by the plan so that the dropped tail
-// of the impulse response is below 1e-9 of its l1 norm (R22).  The
-// look-ahead tile is landed by TMA at the start of a step and reduced at its end;
-// each tile is landed a second time (L2 hit) when it becomes the current tile.
+// of the impulse response is below 1e-9 of its l1 norm (R22).
+// Delayed finalisation: each raw tile t is landed by TMA once; its "front" step
+// runs both recursions with zero anticausal state at the tile's right edge, keeps
+// agg[t] (chunk 0's inclusive suffix state) in a shared-memory ring and parks the
+// partial output P(t) = y+ + y-_0 in tensor memory (tcgen05.st, 32 columns of the
+// thread's own lane).  D steps later its "back" step loads P(t) (tcgen05.ld), adds
+// the anticausal homogeneous response of the carry (plan table GA, packed FFMA2)
+// and hands F(t) to the FHT steps.  No tile is reduced twice.
 //
 // FHT items.  A radix-2^R step after l levels computes, for 2^R consecutive
 // blocks of 2^l rows and one channel c (PAPER.md recursion):
@@ -35,6 +40,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 // Developer timing mask (env FBP_DBG, tools/dev_timing.py: skip TMA loads / FHT
 // steps / epilogue to attribute time) -- compiled in only with -DFBP_DEV_MASK=1
@@ -296,11 +303,17 @@ __device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], flo
 }  // namespace
 
 // ===========================================================================
-// Pass A sweep.  Threads NT = H*X/32 = 128.  Shared memory (floats):
-//   F0, F1 : H x PF  filtered tile (double buffer; landing target), virtual core
-//            columns [HF, HF+X), halo [0, HF) = previous tile's last HF columns
+// Pass A sweep.  Threads NT = H*X/32 = 128 (thread = one 32-sample chunk of a row
+// in the IIR, one register item in the FHT steps).  Shared memory (floats):
+//   F      : H x PF  landing target of raw tile t (TMA box, columns tX-8 ..
+//            tX+X+4) and, once the IIR has read it, the filtered tile F(t-D):
+//            halo [0, HF) = F(t-D-1)'s last HF columns, core [HF, HF+X)
+//   stash  : H x HF  the core's last HF columns (halo of the next F tile)
 //   S1     : H x PS  step-1 output, core [HS, HS+X), halo [0, HS)
-//   ring   : (D+1) x H x 4  anticausal tile aggregates
+//   ring   : (D+1) x H x 3  anticausal tile aggregates agg[t]
+// Tensor memory (IIR): (D+1) slots x 32 columns per thread (its own lane): the
+// tile's partial output P(t) = y+(t) + y-_0(t), y-_0 with zero anticausal state at
+// the tile's right edge, waiting D tiles for its anticausal carry.
 // ===========================================================================
 // S1 halo copy plan of the sweep: row (b', c) of step 2 reads S1 virtual columns
 // >= HS - O2 - c*b' only, so at the end of a tile only the quads
@@ -335,11 +348,36 @@ struct HaloTab {
 template <int H, int HS, int O2, int PS, int NT>
 __device__ constexpr HaloTab<H, HS, O2, PS, NT> kHaloTab{};
 
+// ---- tensor memory (tcgen05): one 32-column slot of a thread's own lane ----
+__device__ __forceinline__ void tmem_st32(unsigned taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;\n"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+        "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]), "=f"(v[16]),
+        "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]),
+        "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
 template <int H, int X, bool IIR, bool BETA>
 __global__ void __launch_bounds__(H * X / 32, 3)
-    k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k,
-              int slices, int f0, int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
-              const __grid_constant__ CUtensorMap tmapF, const __grid_constant__ CUtensorMap tmapL) {
+    k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k, int slices, int f0,
+              int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
+              const __grid_constant__ CUtensorMap tmapF) {
   constexpr int NT = H * X / 32;
   constexpr int TPR = X / 32;                 // chunks (threads) per row in the IIR
   constexpr int R2 = (H == 64) ? 3 : 2;       // k1 = 3 + R2
@@ -351,28 +389,38 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);   // step-2 input halo
   constexpr int PF = pitch4(HF + X + 4);
   constexpr int PS = pitch4(HS + X + 4);
-  constexpr int PL = pitch4(X + 4);                     // look-ahead slot pitch
-  // single F tile + an 8-column halo stash (the next tile's landing overwrites F)
-  constexpr int oF = 0, oStash = H * PF, oS = oStash + H * HF, oLA = oS + H * PS, oRing = oLA + H * PL;
+  constexpr int oF = 0, oStash = H * PF, oS = oStash + H * HF, oRing = oS + H * PS;
   static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
+  static_assert(NT == 128, "TMEM lanes: one per thread");
 
   const int tid = threadIdx.x;
-  const int D = g.D;
+  const int D = IIR ? g.D : 0;
   const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
   using HT = HaloTab<H, HS, O2, PS, NT>;
   unsigned hoff[HT::NKH];                                // this thread's S1 halo quads
 #pragma unroll
   for (int kk = 0; kk < HT::NKH; ++kk) hoff[kk] = kHaloTab<H, HS, O2, PS, NT>.v[kk * NT + tid];
-  // 3 mbarriers (F tile, look-ahead slot, prologue temp in S1), then the work item
+  // 1 mbarrier (F landing), the work item, the TMEM base address
   const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
-  int* s_item = reinterpret_cast<int*>(sm + oBar + 6);
+  int* s_item = reinterpret_cast<int*>(sm + oBar + 2);
+  unsigned* s_tmem = reinterpret_cast<unsigned*>(sm + oBar + 3);
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
+    mbar_init(smem_u32(oBar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (IIR && tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(oBar + 3)),
+                 "r"(g.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  unsigned ph = 0;                                       // phase bits of the 3 mbarriers
-  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt, WR = g.WR;
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // this thread's TMEM lane: warp w owns lanes 32w .. 32w + 31
+  const unsigned tbase = IIR ? (*s_tmem + ((unsigned)(tid & ~31) << 16)) : 0u;
+  unsigned ph = 0;                                       // phase bit of the mbarrier
+  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt;
   const long long nsf = (long long)slices * nf;
   const long long nitems = nsf * NB * nseg;
   // IIR roles: a quarter-warp = 8 rows x the same chunk (conflict-free), the TPR
@@ -397,322 +445,297 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     const long long s = sfi / nf;
     const int fi = (int)(sfi - s * nf);
     const int f = f0 + fi;
-    const float* src = lin + s * lin_slice_stride + ((long long)fi * N + (long long)b * H) * W;
     // compact R layout [slice][family][cf][b][WR]: pass B reads, for one channel cf,
     // the NB rows b as one contiguous box
-    float* dstR = Rout + (((s * 4 + f) * (long long)H) * NB + b) * WR;
+    float* dstR = Rout + (((s * 4 + f) * (long long)H) * NB + b) * g.WR;
     // First tile with an output pass B reads: every stored R column u >= N - b*H
-    // depends on F at u - (H-1) >= N - (b+1)H + 1 only.  The sweep starts D tiles
-    // earlier (warm-up tiles: IIR only) so that the causal carry into tile j0
-    // holds every input within D*X samples -- the same tail bound as the
-    // anticausal look-ahead (R22); linogram rows need not be zero left of N - t
+    // depends on F at u - (H-1) >= N - (b+1)H + 1 only.  The IIR starts D tiles
+    // earlier (causal warm-up, R22): linogram rows need not be zero left of N - t
     // (noisy inputs, configs 2, 4, 5).
     const int j0 = (N - (b + 1) * H + 1) / X;
-    // Segments (small batches, more CTAs than sweeps): segment seg stores the tiles
-    // [ja, jb) of [j0, nt).  It runs step 1 from j1 = ja - 1 (the S1 halo of tile ja
-    // is tile ja - 1's step-1 output; segment 0 needs none, as above) and its IIR
-    // from D tiles before j1 -- the same warm-up / look-ahead bound (R22) as the
-    // sweep's first tile.
+    // Segments (small batches): segment seg stores the tiles [ja, jb) of [j0, nt);
+    // it runs step 1 from j1 = ja - 1 (the S1 halo of tile ja; segment 0 needs none)
     const int seglen = (nt - j0 + nseg - 1) / nseg;
     const int ja = j0 + seg * seglen, jb = min(nt, ja + seglen);
     if (ja >= jb) continue;
     const int j1 = (seg == 0) ? j0 : ja - 1;
+    // front tiles t (IIR of raw tile t) run D tiles ahead of the back tiles j = t - D
+    // (anticausal carry of tile j from agg[j+1 .. j+D], R22; F(j) -> FHT)
     const int jst = IIR ? max(0, j1 - D) : j1;
+    const int tend = jb + D;
 
-    // TMA landings (thread 0 issues; every thread waits on the mbarrier):
-    //   F tile : box of H rows x PF columns from column jt*X - 8 (halo room, left
-    //            neighbour quad, core, right neighbour quad; zero-filled outside the row)
-    //   look-ahead: box of H rows x PL columns from column jt*X
     const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
-    auto tma_issue = [&](const CUtensorMap* mp, int ob, int col, unsigned bytes, int bi) {
+    auto land = [&](int jt) {
       if (tid == 0 && !(dbgm & 8)) {
         fence_proxy_async();
-        const unsigned bar = smem_u32(oBar + 2 * bi);
-        mbar_expect_tx(bar, bytes);
-        tma_load_2d(smem_u32(ob), mp, col, trow, bar);
+        const unsigned bar = smem_u32(oBar);
+        mbar_expect_tx(bar, H * PF * 4);
+        tma_load_2d(smem_u32(oF), &tmapF, jt * X - 8, trow, bar);
       }
     };
-    auto tma_wait = [&](int bi) {
-      if (!(dbgm & 8)) mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1);
-      ph ^= 1u << bi;
+    auto tma_wait = [&]() {
+      if (!(dbgm & 8)) mbar_wait(smem_u32(oBar), ph & 1);
+      ph ^= 1u;
     };
-    auto land = [&](int jt) { tma_issue(&tmapF, oF, jt * X - 8, H * PF * 4, 0); };
-    auto la_land = [&](int ob, int pl, int jt, int bi) {
-      (void)pl;
-      if (jt < nt) tma_issue(&tmapL, ob, jt * X, H * PL * 4, bi);
+    // L2 prefetch of raw tile jt (TMA, no shared memory): the landing of a tile is
+    // issued one step ahead, its first touch of HBM PF tiles ahead
+    constexpr int PFD = 4;
+    auto prefetch = [&](int jt) {
+      if (tid == 0 && jt < nt && !(dbgm & 8)) tma_prefetch_2d(&tmapF, jt * X - 8, trow);
     };
-
-    // look-ahead: anticausal aggregate of landed tile jt -> ring slot
-    auto la_finish = [&](int ob, int pl, int jt, int slot) {
-      const int rowL = ob + ir * pl + 32 * iq;
-      float lx[32];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = ld4(rowL + 4 * q);
-        lx[4 * q] = v.x;
-        lx[4 * q + 1] = v.y;
-        lx[4 * q + 2] = v.z;
-        lx[4 * q + 3] = v.w;
-      }
-      const float4 nx = ld4(rowL + 32);        // next chunk (or next tile) first samples
-      float va[3];
-      chunk_anticausal_state<BETA>(lx, nx.x, nx.y, k, va);
-      // suffix combine over the row's chunks: agg = sum_q (A^32)^q va_q
-      float S0 = va[0], S1v = va[1], S2 = va[2];
-#pragma unroll
-      for (int st = 0; (1 << st) < TPR; ++st) {
-        const int off = 8 << st;
-        const float o[3] = {__shfl_down_sync(0xffffffffu, S0, off), __shfl_down_sync(0xffffffffu, S1v, off),
-                            __shfl_down_sync(0xffffffffu, S2, off)};
-        float t[3] = {0.f, 0.f, 0.f};
-        if (st == 0) mv1(k.M1, o, t);
-        else mv1(k.M2, o, t);
-        if (iq + (1 << st) < TPR) {
-          S0 += t[0];
-          S1v += t[1];
-          S2 += t[2];
-        }
-      }
-      if (iq == 0) {
-        const bool live = jt < nt;
-        const int o = oRing + (slot * H + ir) * 3;
-        sm[o] = live ? S0 : 0.f;
-        sm[o + 1] = live ? S1v : 0.f;
-        sm[o + 2] = live ? S2 : 0.f;
-      }
-    };
-
-    // ---- prologue ----
-    {
-      // L2 prefetch of the sweep's first tiles (one 128-byte line per thread per step)
-      const int je = min(nt, jst + (IIR ? D + 1 : 0) + 1);
-      constexpr int LPR = X / 32;                       // lines per row per tile
-      for (int e = tid; e < H * LPR * (je - jst); e += NT) {
-        const int r = e % H, rest = e / H;
-        prefetch_line(src + (long long)r * W + jst * X + 32 * rest);
-      }
-    }
     land(jst);
-    float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
-    if (IIR) {
-      // prologue look-ahead: tiles jst+1 .. jst+D in batches of two buffers
-      // (LA slot and S1 are free before the first step)
-      for (int i0 = 1; i0 <= D; i0 += 2) {
-        const int nb = min(2, D - i0 + 1);
-        for (int k2 = 0; k2 < nb; ++k2) la_land(k2 == 0 ? oLA : oS, PL, jst + i0 + k2, k2 == 0 ? 1 : 2);
-        for (int k2 = 0; k2 < nb; ++k2)
-          if (jst + i0 + k2 < nt) tma_wait(k2 == 0 ? 1 : 2);
-        for (int k2 = 0; k2 < nb; ++k2)
-          la_finish(k2 == 0 ? oLA : oS, PL, jst + i0 + k2, i0 + k2);   // tile jst+i -> slot i
-        __syncthreads();
-      }
+    for (int i = 1; i <= PFD; ++i) prefetch(jst + i);
+    // S1 halo of the first stored tile: zero (its outputs are never read, but keep
+    // them finite)
+    for (int e = tid; e < H * (HS / 4); e += NT) {
+      const int r = e / (HS / 4), qd = e - r * (HS / 4);
+      st4(oS + r * PS + 4 * qd, make_float4(0.f, 0.f, 0.f, 0.f));
     }
-    int slot_j = 0;                                    // ring slot of tile j (j - jst mod D+1)
+    float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
+    int slot_t = 0;                                      // ring / TMEM slot of tile t: (t - jst) mod (D+1)
 
-    for (int j = jst; j < jb; ++j) {
-      const int oFc = oF;
-      const int jl = j + D + 1;
-
-      tma_wait(0);                                      // F tile of step j landed (each thread)
-
+    for (int t = jst; t < tend; ++t, slot_t = (slot_t == D) ? 0 : slot_t + 1) {
+      const int j = t - D;
+      const bool back = j >= j1;
       if (IIR) {
-        // ---- local sweeps of this thread's chunk ----
-        const int rowF = oFc + ir * PF + HF + 32 * iq;
-        float x[32];
+        if (t < nt) tma_wait();                          // raw tile t landed
+        if (t < nt && !(dbgm & 32)) {
+          // ---- front: zero-state sweeps of this thread's chunk ----
+          const int rowF = oF + ir * PF + HF + 32 * iq;
+          float x[32];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 v = ld4(rowF + 4 * q);
-          x[4 * q] = v.x;
-          x[4 * q + 1] = v.y;
-          x[4 * q + 2] = v.z;
-          x[4 * q + 3] = v.w;
-        }
-        const float4 vl = ld4(rowF - 4);
-        const float4 vr = ld4(rowF + 32);
-        float2 yp[32];
-        chunk_sweep<BETA>(x, vl.w, vl.z, vr.x, vr.y, k, yp);
-        // anticausal carry into this tile's right edge (Horner over the ring)
-        float tm[3];
-        {
-          int sl = slot_j + D;                             // slot of tile j + D
-          if (sl > D) sl -= D + 1;
-          tm[0] = sm[oRing + (sl * H + ir) * 3];
-          tm[1] = sm[oRing + (sl * H + ir) * 3 + 1];
-          tm[2] = sm[oRing + (sl * H + ir) * 3 + 2];
-          for (int i = D - 1; i >= 1; --i) {
-            sl = (sl == 0) ? D : sl - 1;                     // slot of tile j + i
-            float acc[3] = {sm[oRing + (sl * H + ir) * 3], sm[oRing + (sl * H + ir) * 3 + 1],
-                            sm[oRing + (sl * H + ir) * 3 + 2]};
-            mv1(k.MX, tm, acc);
-            tm[0] = acc[0];
-            tm[1] = acc[1];
-            tm[2] = acc[2];
+          for (int q = 0; q < 8; ++q) {
+            const float4 v = ld4(rowF + 4 * q);
+            x[4 * q] = v.x;
+            x[4 * q + 1] = v.y;
+            x[4 * q + 2] = v.z;
+            x[4 * q + 3] = v.w;
           }
-        }
-        // ---- carries: inclusive scan over the row's chunks (causal up, anticausal down)
-        P3 S;
-        S.s0 = make_float2(yp[31].x, yp[31].y);
-        S.s1 = make_float2(yp[30].x, yp[30].y);
-        S.s2 = make_float2(yp[29].x, yp[29].y);
-        {
-          P3 E;
-          E.s0 = make_float2(cin0, tm[0]);
-          E.s1 = make_float2(cin1, tm[1]);
-          E.s2 = make_float2(cin2, tm[2]);
-          const P3 ME = mv(k.M1, E);
+          const float4 vl = ld4(rowF - 4);
+          const float4 vr = ld4(rowF + 32);
+          float2 yp[32];
+          chunk_sweep<BETA>(x, vl.w, vl.z, vr.x, vr.y, k, yp);
+          // carries: inclusive scan over the row's chunks, causal up (seeded with the
+          // exact carry of the previous tile), anticausal down with zero state at the
+          // tile's right edge (its true carry is added D tiles later)
+          P3 S;
+          S.s0 = make_float2(yp[31].x, yp[31].y);
+          S.s1 = make_float2(yp[30].x, yp[30].y);
+          S.s2 = make_float2(yp[29].x, yp[29].y);
           if (iq == 0) {
+            P3 E;
+            E.s0 = make_float2(cin0, 0.f);
+            E.s1 = make_float2(cin1, 0.f);
+            E.s2 = make_float2(cin2, 0.f);
+            const P3 ME = mv(k.M1, E);
             S.s0.x += ME.s0.x;
             S.s1.x += ME.s1.x;
             S.s2.x += ME.s2.x;
           }
-          if (iq == TPR - 1) {
-            S.s0.y += ME.s0.y;
-            S.s1.y += ME.s1.y;
-            S.s2.y += ME.s2.y;
-          }
-        }
 #pragma unroll
-        for (int st = 0; (1 << st) < TPR; ++st) {
-          const int off = 8 << st;
-          P3 o;
-          o.s0 = make_float2(__shfl_up_sync(0xffffffffu, S.s0.x, off), __shfl_down_sync(0xffffffffu, S.s0.y, off));
-          o.s1 = make_float2(__shfl_up_sync(0xffffffffu, S.s1.x, off), __shfl_down_sync(0xffffffffu, S.s1.y, off));
-          o.s2 = make_float2(__shfl_up_sync(0xffffffffu, S.s2.x, off), __shfl_down_sync(0xffffffffu, S.s2.y, off));
-          const P3 t = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
-          if (iq >= (1 << st)) {
-            S.s0.x += t.s0.x;
-            S.s1.x += t.s1.x;
-            S.s2.x += t.s2.x;
+          for (int st = 0; (1 << st) < TPR; ++st) {
+            const int off = 8 << st;
+            P3 o;
+            o.s0 = make_float2(__shfl_up_sync(0xffffffffu, S.s0.x, off), __shfl_down_sync(0xffffffffu, S.s0.y, off));
+            o.s1 = make_float2(__shfl_up_sync(0xffffffffu, S.s1.x, off), __shfl_down_sync(0xffffffffu, S.s1.y, off));
+            o.s2 = make_float2(__shfl_up_sync(0xffffffffu, S.s2.x, off), __shfl_down_sync(0xffffffffu, S.s2.y, off));
+            const P3 tt = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
+            if (iq >= (1 << st)) {
+              S.s0.x += tt.s0.x;
+              S.s1.x += tt.s1.x;
+              S.s2.x += tt.s2.x;
+            }
+            if (iq + (1 << st) < TPR) {
+              S.s0.y += tt.s0.y;
+              S.s1.y += tt.s1.y;
+              S.s2.y += tt.s2.y;
+            }
           }
-          if (iq + (1 << st) < TPR) {
-            S.s0.y += t.s0.y;
-            S.s1.y += t.s1.y;
-            S.s2.y += t.s2.y;
+          // exclusive carries of this chunk
+          P3 cc;
+          {
+            const float u0 = __shfl_up_sync(0xffffffffu, S.s0.x, 8);
+            const float u1 = __shfl_up_sync(0xffffffffu, S.s1.x, 8);
+            const float u2 = __shfl_up_sync(0xffffffffu, S.s2.x, 8);
+            const float d0 = __shfl_down_sync(0xffffffffu, S.s0.y, 8);
+            const float d1 = __shfl_down_sync(0xffffffffu, S.s1.y, 8);
+            const float d2 = __shfl_down_sync(0xffffffffu, S.s2.y, 8);
+            cc.s0 = make_float2(iq == 0 ? cin0 : u0, iq == TPR - 1 ? 0.f : d0);
+            cc.s1 = make_float2(iq == 0 ? cin1 : u1, iq == TPR - 1 ? 0.f : d1);
+            cc.s2 = make_float2(iq == 0 ? cin2 : u2, iq == TPR - 1 ? 0.f : d2);
           }
-        }
-        // exclusive carries of this chunk
-        P3 cc;
-        {
-          const float u0 = __shfl_up_sync(0xffffffffu, S.s0.x, 8);
-          const float u1 = __shfl_up_sync(0xffffffffu, S.s1.x, 8);
-          const float u2 = __shfl_up_sync(0xffffffffu, S.s2.x, 8);
-          const float d0 = __shfl_down_sync(0xffffffffu, S.s0.y, 8);
-          const float d1 = __shfl_down_sync(0xffffffffu, S.s1.y, 8);
-          const float d2 = __shfl_down_sync(0xffffffffu, S.s2.y, 8);
-          cc.s0 = make_float2(iq == 0 ? cin0 : u0, iq == TPR - 1 ? tm[0] : d0);
-          cc.s1 = make_float2(iq == 0 ? cin1 : u1, iq == TPR - 1 ? tm[1] : d1);
-          cc.s2 = make_float2(iq == 0 ? cin2 : u2, iq == TPR - 1 ? tm[2] : d2);
-        }
-        // causal carry for the next tile: inclusive state of the row's last chunk
-        {
-          const int srcl = (lane & 7) | (8 * (TPR - 1)) | (lane & ~(8 * TPR - 1));
-          cin0 = __shfl_sync(0xffffffffu, S.s0.x, srcl);
-          cin1 = __shfl_sync(0xffffffffu, S.s1.x, srcl);
-          cin2 = __shfl_sync(0xffffffffu, S.s2.x, srcl);
-        }
-        // ---- fix-up: add the homogeneous response to the carry-in state, run as the
-        //      zero-input recursion from (cc) -- h_i = (A^(i+1) cc)_0, packed ----
-        {
-          float2 h1 = cc.s0, h2 = cc.s1, h3 = cc.s2;
+          // causal carry for the next tile: inclusive state of the row's last chunk;
+          // agg[t] (anticausal zero-state state at the tile's left edge) = chunk 0's
+          // inclusive suffix state
+          {
+            const int srcl = (lane & 7) | (8 * (TPR - 1)) | (lane & ~(8 * TPR - 1));
+            cin0 = __shfl_sync(0xffffffffu, S.s0.x, srcl);
+            cin1 = __shfl_sync(0xffffffffu, S.s1.x, srcl);
+            cin2 = __shfl_sync(0xffffffffu, S.s2.x, srcl);
+          }
+          if (iq == 0) {
+            const int o = oRing + (slot_t * H + ir) * 3;
+            sm[o] = S.s0.y;
+            sm[o + 1] = S.s1.y;
+            sm[o + 2] = S.s2.y;
+          }
+          // fix-up with the in-tile carries: homogeneous response of the recursion
+          // from the carry-in state, packed (.x causal, .y anticausal).  (A plan-table
+          // form, 3 FFMA2 per sample without the chain, measured slower: r02.)
+          {
+            float2 h1 = cc.s0, h2 = cc.s1, h3 = cc.s2;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float2 h = __fmul2_rn(k.na3, h3);
-            h = __ffma2_rn(k.na2, h2, h);
-            h = __ffma2_rn(k.na1, h1, h);
-            h3 = h2;
-            h2 = h1;
-            h1 = h;
-            yp[i] = __fadd2_rn(yp[i], h);
+            for (int i = 0; i < 32; ++i) {
+              float2 h = __fmul2_rn(k.na3, h3);
+              h = __ffma2_rn(k.na2, h2, h);
+              h = __ffma2_rn(k.na1, h1, h);
+              h3 = h2;
+              h2 = h1;
+              h1 = h;
+              yp[i] = __fadd2_rn(yp[i], h);
+            }
           }
-        }
-        __syncthreads();   // every raw read of this tile (and of the previous look-ahead) is done
-        la_land(oLA, PL, jl, 1);                        // reduced at the end of this step
-        // halo: previous tile's last HF filtered columns (zero before the first tile)
-        for (int e = tid; e < 2 * H; e += NT) {
-          const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
-          st4(oFc + r * PF + 4 * qd, h);
-        }
+          // P(t) = y+ + y-_0 -> tensor memory slot
+          // (the slot's previous content, P(t - D - 1), was loaded by the last back step)
+          float P[32];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int i = 4 * q;
-          st4(rowF + i, make_float4(yp[i].x + yp[31 - i].y, yp[i + 1].x + yp[30 - i].y,
-                                    yp[i + 2].x + yp[29 - i].y, yp[i + 3].x + yp[28 - i].y));
+          for (int i = 0; i < 32; ++i) P[i] = yp[i].x + yp[31 - i].y;
+          tmem_st32(tbase + 32u * slot_t, P);
+        } else if (iq == 0) {                            // beyond the row: agg = 0
+          const int o = oRing + (slot_t * H + ir) * 3;
+          sm[o] = 0.f;
+          sm[o + 1] = 0.f;
+          sm[o + 2] = 0.f;
+        }
+        __syncthreads();                                 // raw tile read, ring written
+        if (back && !(dbgm & 64)) {
+          // ---- back: F(j) = P(j) + anticausal homogeneous response of the carry ----
+          // T_j = sum_{i=1..D} (A^X)^(i-1) agg[j+i] at tile j's right edge (Horner)
+          float tm[3];
+          {
+            int sl = slot_t;                             // slot of tile j + D = t
+            tm[0] = sm[oRing + (sl * H + ir) * 3];
+            tm[1] = sm[oRing + (sl * H + ir) * 3 + 1];
+            tm[2] = sm[oRing + (sl * H + ir) * 3 + 2];
+            for (int i = D - 1; i >= 1; --i) {
+              sl = (sl == 0) ? D : sl - 1;               // slot of tile j + i
+              float acc[3] = {sm[oRing + (sl * H + ir) * 3], sm[oRing + (sl * H + ir) * 3 + 1],
+                              sm[oRing + (sl * H + ir) * 3 + 2]};
+              mv1(k.MX, tm, acc);
+              tm[0] = acc[0];
+              tm[1] = acc[1];
+              tm[2] = acc[2];
+            }
+          }
+          // carry at this chunk's right edge: A^(32 (TPR-1-iq)) T_j
+#pragma unroll
+          for (int q = 0; q < TPR - 1; ++q) {
+            if (q < TPR - 1 - iq) {
+              float acc[3] = {0.f, 0.f, 0.f};
+              mv1(k.M1, tm, acc);
+              tm[0] = acc[0];
+              tm[1] = acc[1];
+              tm[2] = acc[2];
+            }
+          }
+          float P[32];
+          tmem_wait_st();
+          tmem_ld32(tbase + 32u * (slot_t == D ? 0 : slot_t + 1), P);   // slot of tile j = t - D
+          // homogeneous anticausal response at sample i: sum_m (A^(32-i))_{0m} tm_m,
+          // adjacent samples packed (plan table k.GA)
+          const float2 t0 = make_float2(tm[0], tm[0]), t1 = make_float2(tm[1], tm[1]),
+                       t2 = make_float2(tm[2], tm[2]);
+          const int rowF = oF + ir * PF + HF + 32 * iq;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float2 a = make_float2(P[4 * q], P[4 * q + 1]);
+            float2 c = make_float2(P[4 * q + 2], P[4 * q + 3]);
+            a = __ffma2_rn(k.GA[2 * q][0], t0, a);
+            a = __ffma2_rn(k.GA[2 * q][1], t1, a);
+            a = __ffma2_rn(k.GA[2 * q][2], t2, a);
+            c = __ffma2_rn(k.GA[2 * q + 1][0], t0, c);
+            c = __ffma2_rn(k.GA[2 * q + 1][1], t1, c);
+            c = __ffma2_rn(k.GA[2 * q + 1][2], t2, c);
+            st4(rowF + 4 * q, make_float4(a.x, a.y, c.x, c.y));
+          }
         }
       } else {
+        tma_wait();                                      // raw tile j = F(j) landed
+      }
+      if (back) {
+        // halo: F(j-1)'s last HF columns (zero at the first back tile)
         for (int e = tid; e < 2 * H; e += NT) {
           const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == jst) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
-          st4(oFc + r * PF + 4 * qd, h);
+          const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
+          st4(oF + r * PF + 4 * qd, h);
         }
       }
-      __syncthreads();                                   // F tile complete
-
-      // ---- FHT step 1 (levels 1-3): F -> S1 ----
-      if (j >= j1) {
+      __syncthreads();                                   // F(j) complete
+      if (back && !(dbgm & 1)) {
+        // ---- FHT step 1 (levels 1-3): F -> S1 ----
         constexpr int NCH = X / C1;
         const int jj = tid % NCH, G = tid / NCH;
         float2 v[8][It<3, C1>::T / 2];
-        item_load<3, C1>(oFc + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
+        item_load<3, C1>(oF + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
         item_fht<3, C1>(v);
         const int gb = G & (NR2 - 1);                   // next step's block index
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int o = oS + (G * 8 + r) * PS + HS + C1 * jj + ((r * gb) & 3);
 #pragma unroll
-          for (int t = 0; t < C1; ++t) sm[o + t] = col(v[r], It<3, C1>::O + t);
+          for (int tt = 0; tt < C1; ++tt) sm[o + tt] = col(v[r], It<3, C1>::O + tt);
+        }
+        // stash this tile's last HF filtered columns (halo of the next tile)
+        for (int e = tid; e < 2 * H; e += NT) {
+          const int r = e >> 1, qd = e & 1;
+          st4(oStash + r * HF + 4 * qd, ld4(oF + r * PF + X + 4 * qd));
         }
       }
-      // stash this tile's last HF filtered columns (halo of the next tile)
-      for (int e = tid; e < 2 * H; e += NT) {
-        const int r = e >> 1, qd = e & 1;
-        st4(oStash + r * HF + 4 * qd, ld4(oFc + r * PF + X + 4 * qd));
-      }
       __syncthreads();
-      if (j + 1 < jb) land(j + 1);                       // F is free: step 1 has read it
-      // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
-      // Items whose NR2 channels cf = c*NR2 + r need none of their columns (u outside
-      // [N - b(cf+1), 2N - cf*b) for every r) are skipped: up to half of them for
-      // the high blocks b.
-      constexpr int NCH2 = X / C2;
-      const int ub2 = j * X + C2 * (tid % NCH2), c2 = tid / NCH2;
-      const bool need2 = (ub2 + C2 > N - b * (c2 * NR2 + NR2)) && (ub2 < W - c2 * NR2 * b);
-      if (j >= ja && need2) {
-        constexpr int NCH = X / C2;
-        const int jj = tid % NCH, c = tid / NCH;
-        float2 v[NR2][It<R2, C2>::T / 2];
-        item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
-        item_fht<R2, C2>(v);
+      // F is free: land the next raw tile
+      if (IIR) {
+        if (t + 1 < nt && t + 1 < tend) land(t + 1);
+        prefetch(t + 1 + PFD);
+      } else if (j + 1 < jb) {
+        land(j + 1);
+        if (j + 1 + PFD < jb) prefetch(j + 1 + PFD);
+      }
+      if (back && j >= ja && !(dbgm & 2)) {
+        // ---- FHT step 2 (levels 4..k1): S1 -> R (compact, only the columns pass B reads)
+        // Items whose NR2 channels cf = c*NR2 + r need none of their columns (u outside
+        // [N - b(cf+1), 2N - cf*b) for every r) are skipped: up to half of them for
+        // the high blocks b.
+        constexpr int NCH2 = X / C2;
+        const int jj = tid % NCH2, c = tid / NCH2;
         const int ubase = j * X + C2 * jj;
+        const bool need2 = (ubase + C2 > N - b * (c * NR2 + NR2)) && (ubase < W - c * NR2 * b);
+        if (need2) {
+          float2 v[NR2][It<R2, C2>::T / 2];
+          item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
+          item_fht<R2, C2>(v);
 #pragma unroll
-        for (int r = 0; r < NR2; ++r) {
-          const int cf = c * NR2 + r;
-          const int ulo = N - b * (cf + 1);
-          const int uhi = W - cf * b;
-          float* o = dstR + (long long)cf * NB * WR + (cf * b - N + NB);
-          if (ubase >= ulo && ubase + C2 <= uhi) {
+          for (int r = 0; r < NR2; ++r) {
+            const int cf = c * NR2 + r;
+            const int ulo = N - b * (cf + 1);
+            const int uhi = W - cf * b;
+            float* o = dstR + (long long)cf * NB * g.WR + (cf * b - N + NB);
+            if (ubase >= ulo && ubase + C2 <= uhi) {
 #pragma unroll
-            for (int t = 0; t < C2; ++t) st_ef(o + ubase + t, col(v[r], O2 + t), pol_ef);
-          } else if (ubase + C2 > ulo && ubase < uhi) {
+              for (int tt = 0; tt < C2; ++tt) st_ef(o + ubase + tt, col(v[r], O2 + tt), pol_ef);
+            } else if (ubase + C2 > ulo && ubase < uhi) {
 #pragma unroll
-            for (int t = 0; t < C2; ++t) {
-              const int u = ubase + t;
-              if (u >= ulo && u < uhi) st_ef(o + u, col(v[r], O2 + t), pol_ef);
+              for (int tt = 0; tt < C2; ++tt) {
+                const int u = ubase + tt;
+                if (u >= ulo && u < uhi) st_ef(o + u, col(v[r], O2 + tt), pol_ef);
+              }
             }
           }
         }
       }
-      // look-ahead reduction before the barrier: it needs only the landing (every
-      // thread waits on the mbarrier) and writes ring entries its own warp reads
-      if (IIR && jl < nt) tma_wait(1);
-      if (IIR) la_finish(oLA, PL, jl, slot_j);          // tile j + D + 1 reuses tile j's slot
-      slot_j = (slot_j == D) ? 0 : slot_j + 1;
       __syncthreads();                                   // step 2's S1 reads precede the halo copy
       // ---- S1 halo for the next tile: row (b', c) of step 2 reads virtual columns
       //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
-      // the needed (row, quad) pairs, dealt round-robin to the threads (HaloTab):
-      // at most NKH live quads per thread, all loads issued before the stores
-      if (j >= j1) {
+      if (back) {
         float4 tq[HT::NKH];
 #pragma unroll
         for (int kk = 0; kk < HT::NKH; ++kk)
@@ -723,6 +746,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       }
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (IIR && tid < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(*s_tmem), "r"(g.tmem_cols)
+                 : "memory");
 }
 
 // ===========================================================================
@@ -938,11 +966,10 @@ bool sweep_supported(int N) { return N == 512 || N == 1024 || N == 2048 || N == 
 size_t sweep_a_smem(const SweepGeom& g) {
   const int H = g.H, X = g.X;
   const int R2 = (H == 64) ? 3 : 2;
-  const int O2 = 4;
-  const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : O2 + 4 * ((7 * 3) / 4);
-  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4), PL = pitch4(X + 4);
-  return ((size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)H * PL + (size_t)(g.D + 1) * H * 3 + 4 + 6 +
-          2) * sizeof(float);
+  const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : 4 + 4 * ((7 * 3) / 4);
+  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
+  const size_t fl = (size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 8;
+  return fl * sizeof(float);
 }
 
 size_t pair_b_smem(const SweepGeom& g, int pair) {
@@ -996,31 +1023,61 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
                               long long stride, const SweepGeom& g, const SweepIir& k, int* counter,
                               cudaStream_t st) {
   auto kern = k_sweep_a<H, X, IIR, BETA>;
-  const size_t smem = sweep_a_smem(g);
+  size_t smem = sweep_a_smem(g);
+  // tensor memory: (D+1) slots of 32 columns per lane; never more CTAs per SM than
+  // the 512 columns hold (a CTA waiting in tcgen05.alloc would spin): raise the
+  // shared-memory request so that the occupancy limit enforces it
+  if (IIR) {
+    const int per_tmem = 512 / g.tmem_cols;
+    const size_t cap = (size_t)227 * 1024 / (per_tmem + 1) + 1024;
+    if (per_tmem < 3) smem = std::max(smem, cap);
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, H * X / 32, smem);
+  const cudaError_t eo = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, H * X / 32, smem);
+  cudaGetLastError();
+  {
+    // the occupancy calculator reports 1 CTA/SM for kernels that allocate tensor
+    // memory; the resident limit is set by shared memory, registers and TMEM columns
+    cudaFuncAttributes fa;
+    int smem_sm = 0, regs_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.numRegs > 0) {
+      const int regs_cta = ((fa.numRegs + 7) / 8 * 8) * (H * X / 32);
+      const int by_regs = regs_sm / regs_cta;
+      const int by_smem = (int)(smem_sm / (smem + fa.sharedSizeBytes + 1024));
+      int manual = std::min(by_regs, by_smem);
+      if (IIR) manual = std::min(manual, 512 / g.tmem_cols);
+      if (eo != cudaSuccess || per < manual) per = manual;
+    }
+  }
+  if (IIR) per = std::min(per, 512 / g.tmem_cols);
   if (g.ctas_a > 0 && g.ctas_a < per) per = g.ctas_a;   // tuning knob (FBP_SWEEP_CTAS)
   if (per < 1) per = 1;
   // small batches: split every sweep into segments until there are ~1.7 work items
-  // per resident CTA slot (measured at N = 2048: B = 1 -> 6 segments, 2 -> 3, 4 -> 2,
-  // >= 8 -> 1; FBP_SWEEP_SEG overrides)
+  // per resident CTA slot (measured r01 at N = 2048: B = 1 -> 6 segments, 2 -> 3,
+  // 4 -> 2, >= 8 -> 1; FBP_SWEEP_SEG overrides)
   const long long sweeps = (long long)slices * nf * g.NB;
   const long long slots = (long long)sms * per;
   int nseg = (int)std::min<long long>(8, std::max<long long>(1, (17 * slots + 10 * sweeps - 1) / (10 * sweeps)));
   if (g.nseg > 0) nseg = g.nseg;
   const long long nitems = sweeps * nseg;
   const long long grid = std::min<long long>(nitems, (long long)sms * per);
-  CUtensorMap tF, tL;
+#if FBP_DEV_MASK
+  if (std::getenv("FBP_VERBOSE"))
+    fprintf(stderr, "sweep: smem %zu per %d tmem_cols %d nseg %d grid %lld D %d\n", smem, per, g.tmem_cols, nseg, grid,
+            g.D);
+#endif
+  CUtensorMap tF;
   e = make_lin_map(&tF, lin, slices, g, pitch4(8 + X + 4), H);
-  if (e == cudaSuccess) e = make_lin_map(&tL, lin, slices, g, pitch4(X + 4), H);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, nseg, counter, tF, tL);
+  kern<<<(unsigned)grid, H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, nseg, counter, tF);
   return cudaGetLastError();
 }
 
@@ -1031,6 +1088,7 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
   // the TMA maps address rows (slice*4 + family)*N + t of a contiguous batch
   if (f0 != 0 || nf != 4 || lin_slice_stride != 4LL * g.N * g.W || (reinterpret_cast<uintptr_t>(lin) & 15))
     return cudaErrorInvalidValue;
+  if ((long long)slices * 4 * g.H * g.NB > 0x7fffffffLL) return cudaErrorInvalidValue;
   const bool beta = k.beta.x != 0.0f;
   cudaError_t e;
 #define FBP_SWEEP_CASE(HH, XX)                                                                     \
