@@ -11,5 +11,5 @@ Random numbers the method itself would draw: none (the method is deterministic).
 from .generator import (  # noqa: F401
     CONFIGS, EllipseSet, draw_ellipses, linogram_of_ellipses, add_noise,
     make_slice, make_batch, random_linogram, integer_linogram, integer_image, random_image,
-    sinogram_of_ellipses,
+    sinogram_of_ellipses, image_of_ellipses,
 )

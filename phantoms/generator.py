@@ -192,6 +192,18 @@ def random_image(N: int, batch: int, seed: int, device="cpu") -> torch.Tensor:
     return x.to(torch.float32).to(device)
 
 
+def image_of_ellipses(E: EllipseSet, N: int) -> np.ndarray:
+    """The ellipse phantom sampled at pixel centres (x + 0.5, y + 0.5), img[y][x],
+    float64 (reference image of the NEXT-3/NEXT-4 quality studies)."""
+    yy, xx = np.mgrid[0:N, 0:N] + 0.5
+    img = np.zeros((N, N))
+    for cx, cy, a, b, phi, rho in zip(E.cx, E.cy, E.a, E.b, E.phi, E.rho):
+        u = (xx - cx) * np.cos(phi) + (yy - cy) * np.sin(phi)
+        v = -(xx - cx) * np.sin(phi) + (yy - cy) * np.cos(phi)
+        img += rho * ((u / a) ** 2 + (v / b) ** 2 <= 1.0)
+    return img
+
+
 def sinogram_of_ellipses(E: EllipseSet, N: int, n_angles: int, n_bins: int, dr: float = 1.0,
                          dtype=torch.float64) -> torch.Tensor:
     """Scanner sinogram p[k][j] of the ellipse phantom (arc-length line integrals,

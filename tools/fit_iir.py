@@ -16,6 +16,8 @@ are produced here once and FROZEN in ``coeffs/*.json`` (reading R13):
 
 Standalone CPU tool: uses scipy only; imports neither ``oracle`` nor the product.
 Usage:  python tools/fit_iir.py --n 64 512 1024 2048 4096 --order 3
+        python tools/fit_iir.py --sweep 1 2 3 4 5 --k 512     (NEXT-3 order sweep,
+            M = Q = q, both variants -> coeffs/sweep/iir_q<q>_<variant>.json)
 """
 from __future__ import annotations
 
@@ -45,8 +47,11 @@ def unpack(p, M, Q, dc0):
     return b, a
 
 
-def fit(K: int, M: int, Q: int, dc0: bool, restarts: int = 8, seed: int = 0):
-    target = half_ramp(K)
+def fit(K: int, M: int, Q: int, dc0: bool, restarts: int = 8, seed: int = 0, target=None):
+    """Nelder-Mead fit of b (M taps), a (Q taps) so that the causal impulse response
+    matches `target` (default: the causal half h+ of the ramp kernel, Eq.10) in
+    least squares over lags 0..K."""
+    target = half_ramp(K) if target is None else np.asarray(target, dtype=np.float64)[: K + 1]
     imp = np.zeros(K + 1)
     imp[0] = 1.0
 
@@ -86,9 +91,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, nargs="+", default=[64, 512, 1024, 2048, 4096])
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--sweep", type=int, nargs="*", default=None, help="orders q of the NEXT-3 sweep")
+    ap.add_argument("--k", type=int, default=512, help="fit range K of the sweep")
     ap.add_argument("--out", default=os.path.join(os.path.dirname(__file__), "..", "coeffs"))
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
+    if args.sweep:
+        out = os.path.join(args.out, "sweep")
+        os.makedirs(out, exist_ok=True)
+        for q in args.sweep:
+            for dc0 in (False, True):
+                r = fit(args.k, q, q, dc0)
+                path = os.path.join(out, f"iir_q{q}_{r['variant']}.json")
+                with open(path, "w") as fh:
+                    json.dump(r, fh, indent=1)
+                print(path, "mse", r["mse"], "max|p|", r["max_pole"], "dc", r["dc_gain"])
+        return
     for N in args.n:
         for dc0 in (False, True):
             r = fit(N, args.order, args.order, dc0)
