@@ -426,20 +426,9 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
           else si.GA[i >> 1][m2].x = (float)Pm[(size_t)m2];
         }
       }
-      for (int i = 0; i < 64; ++i) {   // the same over a 64-sample row (dual-pipeline sweep)
-        matpow(3, A3, 64 - i, Pm);
-        for (int m2 = 0; m2 < 3; ++m2) {
-          if (i & 1) si.GA64[i >> 1][m2].y = (float)Pm[(size_t)m2];
-          else si.GA64[i >> 1][m2].x = (float)Pm[(size_t)m2];
-        }
-      }
       int cols = 32;
       while (cols < 32 * (D + 1)) cols *= 2;
       sg.tmem_cols = cols;
-      sg.ws = 0;   // single-role k_sweep_a (the ws = 1 / 2 variants measured slower)
-#if FBP_DEV_MASK
-      if (const char* ev = std::getenv("FBP_WS")) sg.ws = std::atoi(ev);
-#endif
       p->fast = true;
     }
   }

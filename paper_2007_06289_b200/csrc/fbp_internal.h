@@ -67,9 +67,6 @@ struct SweepIir {
   // homogeneous response at sample i of a 32-sample chunk to the state at the
   // chunk's right edge (adjacent samples packed for FFMA2)
   float2 GA[16][3];
-  // GA64[p][m] = (G64^(2p), G64^(2p+1)), G64^(s) = (A^(64-s))_{0m}: the same response
-  // over a 64-sample tile row (dual-pipeline sweep, thread per row)
-  float2 GA64[32][3];
 };
 
 struct SweepGeom {
@@ -81,8 +78,6 @@ struct SweepGeom {
   int XB;     // pass-B x-tile width
   int ctas_a; // cap on resident sweep CTAs per SM (0: occupancy limit); env FBP_SWEEP_CTAS
   int nseg;   // segments per sweep (0: automatic, fill the CTA slots); env FBP_SWEEP_SEG
-  int ws;         // 2: dual-pipeline sweep (k_sweep_dual, H = 64), 1: warp-specialised
-                  // k_sweep_ws, 0: single-role k_sweep_a
   int tmem_cols;  // tensor-memory columns per sweep CTA: (D+1) x 32 rounded to a power of two
   int dbg;    // developer timing mask, env FBP_DBG, honoured only in -DFBP_DEV_MASK=1 builds
               // (results invalid when nonzero): pass B bit 0

@@ -40,7 +40,6 @@
 #include <cuda.h>
 
 #include <algorithm>
-#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -376,11 +375,6 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
         "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
       : "r"(taddr)
       : "memory");
-}
-__device__ __forceinline__ void tmem_st8(unsigned taddr, const float (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
-               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-               : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -779,786 +773,6 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 }
 
 // ===========================================================================
-// Warp-specialised sweep (fast path with the IIR): the same tiles and arithmetic
-// as k_sweep_a, split over two warpgroups of one CTA so that the recursions and the
-// FHT steps of different tiles overlap (DESIGN.md §6 KS):
-//   WG-I (warps 0-3, thread = one 32-sample chunk of a row): front of raw tile t
-//        (both recursions, TMEM P(t), agg[t]) and back of tile j = t - D (carry,
-//        F(j) -> F buffer); issues the TMA landings of the raw tiles.
-//   WG-F (warps 4-7, thread = one register item): halo, FHT step 1, step 2, R stores,
-//        S1 halo copy.
-// Shared memory: RAW[2] (raw tile landings), F[2] (filtered tiles, WG-I -> WG-F),
-// S1, the agg ring; mbarriers rawfull[2] (TMA), fready[2] (WG-I -> WG-F),
-// ffree[2] (WG-F -> WG-I).  Named barriers 1 (WG-I) and 2 (WG-F); barrier 0 (CTA)
-// only between work items.  Running tile counters (raw landings, F tiles) give
-// every buffer index and mbarrier phase across items.
-// ===========================================================================
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-
-// chunk_sweep with the chunk's 32 samples streamed from shared memory (quads from
-// both ends) instead of held in registers: row = float offset of sample 0.
-template <bool BETA>
-__device__ __forceinline__ void chunk_sweep_smem(int row, const SweepIir& k, float2 (&yp)[32]) {
-  const float4 vl = ld4(row - 4);
-  const float4 vr = ld4(row + 32);
-  float pl = vl.w, pr = vr.x;                            // x[-1], x[32]
-  float2 dprev = make_float2(vl.w - vl.z, vr.x - vr.y);  // (x[-1] - x[-2], x[32] - x[33])
-  float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 a4 = ld4(row + 4 * q);                  // x[4q .. 4q+3]
-    const float4 b4 = ld4(row + 28 - 4 * q);             // x[28-4q .. 31-4q]
-    const float xa[4] = {a4.x, a4.y, a4.z, a4.w};
-    const float xb[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const float xi = xa[u], xim1 = (u == 0) ? pl : xa[u - 1];
-      const float xr = xb[3 - u], xrp1 = (u == 0) ? pr : xb[4 - u];
-      float2 d;
-      d.x = xi - xim1;
-      d.y = xr - xrp1;
-      float2 uu = __fmul2_rn(k.c1, dprev);
-      uu = __ffma2_rn(k.c0, d, uu);
-      if (BETA) {
-        uu.x = fmaf(k.beta.x, xi, uu.x);
-        uu.y = fmaf(k.beta.x, xr, uu.y);
-      }
-      float2 v = __ffma2_rn(k.na3, y3, uu);
-      v = __ffma2_rn(k.na2, y2, v);
-      v = __ffma2_rn(k.na1, y1, v);
-      y3 = y2;
-      y2 = y1;
-      y1 = v;
-      dprev = d;
-      yp[4 * q + u] = v;
-    }
-    pl = xa[3];
-    pr = xb[0];
-  }
-}
-
-template <int H, int X, bool BETA>
-__global__ void __launch_bounds__(2 * H * X / 32, 2)
-    k_sweep_ws(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k, int slices,
-               int f0, int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
-               const __grid_constant__ CUtensorMap tmapF) {
-  constexpr int NW = H * X / 32;              // threads per warpgroup (128)
-  constexpr int TPR = X / 32;
-  constexpr int R2 = (H == 64) ? 3 : 2;
-  constexpr int C1 = 4;
-  constexpr int C2 = (R2 == 3) ? 4 : 8;
-  constexpr int O2 = It<R2, C2>::O;
-  constexpr int NR2 = 1 << R2;
-  constexpr int HF = 8;
-  constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);
-  constexpr int PF = pitch4(HF + X + 4);
-  constexpr int PS = pitch4(HS + X + 4);
-  constexpr int oRaw = 0, oF = 2 * H * PF, oS = oF + 2 * H * PF, oRing = oS + H * PS;
-  static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
-  static_assert(NW == 128, "TMEM lanes: one per IIR thread");
-
-  const int tid = threadIdx.x;
-  const bool wgI = tid < NW;
-  const int wt = wgI ? tid : tid - NW;        // thread index within the warpgroup
-  const int D = g.D;
-  const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
-  using HT = HaloTab<H, HS, O2, PS, NW>;
-  // barriers: rawfull[2], fready[2], ffree[2] (8 bytes each), then item + TMEM base
-  const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
-  auto bar_raw = [&](int i) { return smem_u32(oBar + 2 * i); };
-  auto bar_fready = [&](int i) { return smem_u32(oBar + 4 + 2 * i); };
-  auto bar_ffree = [&](int i) { return smem_u32(oBar + 8 + 2 * i); };
-  int* s_item = reinterpret_cast<int*>(sm + oBar + 12);
-  unsigned* s_tmem = reinterpret_cast<unsigned*>(sm + oBar + 13);
-  if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar_raw(i), 1);
-      mbar_init(bar_fready(i), NW);
-      mbar_init(bar_ffree(i), NW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(oBar + 13)),
-                 "r"(g.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const unsigned tbase = *s_tmem + ((unsigned)(tid & ~31) << 16);   // WG-I lanes 0..127
-  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt;
-  const long long nsf = (long long)slices * nf;
-  const long long nitems = nsf * NB * nseg;
-  const int iq = (wt >> 3) % TPR;
-  const int ir = (wt & 7) + 8 * (wt / (8 * TPR));
-  const int lane = tid & 31;
-  const unsigned long long pol_ef = policy_evict_first();
-  unsigned nraw = 0;     // raw tiles landed by this CTA (WG-I thread 0 issues; all WG-I wait)
-  unsigned nfw = 0;      // F tiles written (WG-I) / consumed (WG-F) by this CTA
-  unsigned hoff[HT::NKH];
-#pragma unroll
-  for (int kk = 0; kk < HT::NKH; ++kk) hoff[kk] = kHaloTab<H, HS, O2, PS, NW>.v[kk * NW + wt];
-
-  while (true) {
-    __syncthreads();
-    if (tid == 0) *s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    const long long item = *s_item;
-    if (item >= nitems) break;
-    const int seg = (int)(item % nseg);
-    const long long it2 = item / nseg;
-    const int b = NB - 1 - (int)(it2 / nsf);
-    const long long sfi = it2 - (long long)(NB - 1 - b) * nsf;
-    const long long s = sfi / nf;
-    const int fi = (int)(sfi - s * nf);
-    const int f = f0 + fi;
-    float* dstR = Rout + (((s * 4 + f) * (long long)H) * NB + b) * g.WR;
-    const int j0 = (N - (b + 1) * H + 1) / X;
-    const int seglen = (nt - j0 + nseg - 1) / nseg;
-    const int ja = j0 + seg * seglen, jb = min(nt, ja + seglen);
-    if (ja >= jb) continue;
-    const int j1 = (seg == 0) ? j0 : ja - 1;
-    const int jst = max(0, j1 - D);
-    const int tend = jb + D;
-    const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
-    const unsigned nraw0 = nraw, nf0 = nfw;   // counters at the item start (both WGs)
-
-    if (wgI) {
-      // ============================ WG-I: recursions ============================
-      auto land = [&](int jt, unsigned n) {   // raw tile jt -> RAW[n & 1]
-        if (wt == 0 && !(dbgm & 8)) {
-          fence_proxy_async();
-          mbar_expect_tx(bar_raw(n & 1), H * PF * 4);
-          tma_load_2d(smem_u32(oRaw + (n & 1) * H * PF), &tmapF, jt * X - 8, trow, bar_raw(n & 1));
-        }
-      };
-      constexpr int PFD = 4;
-      auto prefetch = [&](int jt) {
-        if (wt == 0 && jt < nt && !(dbgm & 8)) tma_prefetch_2d(&tmapF, jt * X - 8, trow);
-      };
-      const int tlast = min(nt, tend);                   // front tiles [jst, tlast)
-      land(jst, nraw0);
-      if (jst + 1 < tlast) land(jst + 1, nraw0 + 1);
-      for (int i = 2; i <= PFD + 1; ++i) prefetch(jst + i);
-      float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;
-      int slot_t = 0;
-      for (int t = jst; t < tend; ++t, slot_t = (slot_t == D) ? 0 : slot_t + 1) {
-        const int j = t - D;
-        if (t < nt) {
-          const unsigned n = nraw;
-          if (!(dbgm & 8)) mbar_wait(bar_raw(n & 1), (n >> 1) & 1);
-          ++nraw;
-          const int rowF = oRaw + (n & 1) * H * PF + ir * PF + HF + 32 * iq;
-          float2 yp[32];
-          chunk_sweep_smem<BETA>(rowF, k, yp);
-          P3 S;
-          S.s0 = make_float2(yp[31].x, yp[31].y);
-          S.s1 = make_float2(yp[30].x, yp[30].y);
-          S.s2 = make_float2(yp[29].x, yp[29].y);
-          if (iq == 0) {
-            P3 E;
-            E.s0 = make_float2(cin0, 0.f);
-            E.s1 = make_float2(cin1, 0.f);
-            E.s2 = make_float2(cin2, 0.f);
-            const P3 ME = mv(k.M1, E);
-            S.s0.x += ME.s0.x;
-            S.s1.x += ME.s1.x;
-            S.s2.x += ME.s2.x;
-          }
-#pragma unroll
-          for (int st = 0; (1 << st) < TPR; ++st) {
-            const int off = 8 << st;
-            P3 o;
-            o.s0 = make_float2(__shfl_up_sync(0xffffffffu, S.s0.x, off), __shfl_down_sync(0xffffffffu, S.s0.y, off));
-            o.s1 = make_float2(__shfl_up_sync(0xffffffffu, S.s1.x, off), __shfl_down_sync(0xffffffffu, S.s1.y, off));
-            o.s2 = make_float2(__shfl_up_sync(0xffffffffu, S.s2.x, off), __shfl_down_sync(0xffffffffu, S.s2.y, off));
-            const P3 tt = (st == 0) ? mv(k.M1, o) : mv(k.M2, o);
-            if (iq >= (1 << st)) {
-              S.s0.x += tt.s0.x;
-              S.s1.x += tt.s1.x;
-              S.s2.x += tt.s2.x;
-            }
-            if (iq + (1 << st) < TPR) {
-              S.s0.y += tt.s0.y;
-              S.s1.y += tt.s1.y;
-              S.s2.y += tt.s2.y;
-            }
-          }
-          P3 cc;
-          {
-            const float u0 = __shfl_up_sync(0xffffffffu, S.s0.x, 8);
-            const float u1 = __shfl_up_sync(0xffffffffu, S.s1.x, 8);
-            const float u2 = __shfl_up_sync(0xffffffffu, S.s2.x, 8);
-            const float d0 = __shfl_down_sync(0xffffffffu, S.s0.y, 8);
-            const float d1 = __shfl_down_sync(0xffffffffu, S.s1.y, 8);
-            const float d2 = __shfl_down_sync(0xffffffffu, S.s2.y, 8);
-            cc.s0 = make_float2(iq == 0 ? cin0 : u0, iq == TPR - 1 ? 0.f : d0);
-            cc.s1 = make_float2(iq == 0 ? cin1 : u1, iq == TPR - 1 ? 0.f : d1);
-            cc.s2 = make_float2(iq == 0 ? cin2 : u2, iq == TPR - 1 ? 0.f : d2);
-          }
-          {
-            const int srcl = (lane & 7) | (8 * (TPR - 1)) | (lane & ~(8 * TPR - 1));
-            cin0 = __shfl_sync(0xffffffffu, S.s0.x, srcl);
-            cin1 = __shfl_sync(0xffffffffu, S.s1.x, srcl);
-            cin2 = __shfl_sync(0xffffffffu, S.s2.x, srcl);
-          }
-          if (iq == 0) {
-            const int o = oRing + (slot_t * H + ir) * 3;
-            sm[o] = S.s0.y;
-            sm[o + 1] = S.s1.y;
-            sm[o + 2] = S.s2.y;
-          }
-          {
-            float2 h1 = cc.s0, h2 = cc.s1, h3 = cc.s2;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float2 h = __fmul2_rn(k.na3, h3);
-              h = __ffma2_rn(k.na2, h2, h);
-              h = __ffma2_rn(k.na1, h1, h);
-              h3 = h2;
-              h2 = h1;
-              h1 = h;
-              yp[i] = __fadd2_rn(yp[i], h);
-            }
-          }
-          float P[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) P[i] = yp[i].x + yp[31 - i].y;
-          tmem_st32(tbase + 32u * slot_t, P);
-          named_sync(1, NW);                             // RAW[n & 1] fully read
-          if (t + 2 < tlast) land(t + 2, n + 2);
-          prefetch(t + 2 + PFD);
-        } else if (iq == 0) {
-          const int o = oRing + (slot_t * H + ir) * 3;
-          sm[o] = 0.f;
-          sm[o + 1] = 0.f;
-          sm[o + 2] = 0.f;
-        }
-        __syncwarp();                                    // ring entries are warp-local
-        if (j >= j1) {
-          float tm[3];
-          {
-            int sl = slot_t;
-            tm[0] = sm[oRing + (sl * H + ir) * 3];
-            tm[1] = sm[oRing + (sl * H + ir) * 3 + 1];
-            tm[2] = sm[oRing + (sl * H + ir) * 3 + 2];
-            for (int i = D - 1; i >= 1; --i) {
-              sl = (sl == 0) ? D : sl - 1;
-              float acc[3] = {sm[oRing + (sl * H + ir) * 3], sm[oRing + (sl * H + ir) * 3 + 1],
-                              sm[oRing + (sl * H + ir) * 3 + 2]};
-              mv1(k.MX, tm, acc);
-              tm[0] = acc[0];
-              tm[1] = acc[1];
-              tm[2] = acc[2];
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < TPR - 1; ++q) {
-            if (q < TPR - 1 - iq) {
-              float acc[3] = {0.f, 0.f, 0.f};
-              mv1(k.M1, tm, acc);
-              tm[0] = acc[0];
-              tm[1] = acc[1];
-              tm[2] = acc[2];
-            }
-          }
-          float P[32];
-          tmem_wait_st();
-          tmem_ld32(tbase + 32u * (slot_t == D ? 0 : slot_t + 1), P);
-          const float2 t0 = make_float2(tm[0], tm[0]), t1 = make_float2(tm[1], tm[1]),
-                       t2 = make_float2(tm[2], tm[2]);
-          // F buffer nfw & 1: wait until WG-F released its previous tile (two back)
-          const unsigned n = nfw++;
-          if (n >= 2) mbar_wait(bar_ffree(n & 1), ((n >> 1) - 1) & 1);
-          const int rowF = oF + (n & 1) * H * PF + ir * PF + HF + 32 * iq;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float2 a = make_float2(P[4 * q], P[4 * q + 1]);
-            float2 c = make_float2(P[4 * q + 2], P[4 * q + 3]);
-            a = __ffma2_rn(k.GA[2 * q][0], t0, a);
-            a = __ffma2_rn(k.GA[2 * q][1], t1, a);
-            a = __ffma2_rn(k.GA[2 * q][2], t2, a);
-            c = __ffma2_rn(k.GA[2 * q + 1][0], t0, c);
-            c = __ffma2_rn(k.GA[2 * q + 1][1], t1, c);
-            c = __ffma2_rn(k.GA[2 * q + 1][2], t2, c);
-            st4(rowF + 4 * q, make_float4(a.x, a.y, c.x, c.y));
-          }
-          mbar_arrive(bar_fready(n & 1));                // release: F(j) written
-        }
-      }
-    } else {
-      // ============================ WG-F: FHT steps =============================
-      // S1 halo of the first stored tile: zero
-      for (int e = wt; e < H * (HS / 4); e += NW) {
-        const int r = e / (HS / 4), qd = e - r * (HS / 4);
-        st4(oS + r * PS + 4 * qd, make_float4(0.f, 0.f, 0.f, 0.f));
-      }
-      for (int j = j1; j < jb; ++j) {
-        const unsigned n = nfw++;
-        mbar_wait(bar_fready(n & 1), (n >> 1) & 1);
-        const int oFc = oF + (n & 1) * H * PF, oFp = oF + ((n + 1) & 1) * H * PF;
-        // halo: F(j-1)'s last HF columns (zero at the first tile of the item)
-        for (int e = wt; e < 2 * H; e += NW) {
-          const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + r * PF + X + 4 * qd);
-          st4(oFc + r * PF + 4 * qd, h);
-        }
-        named_sync(2, NW);                               // F(j) complete; F(j-1) done
-        if (j > j1) mbar_arrive(bar_ffree((n + 1) & 1)); // release F(j-1)'s buffer
-        if (!(dbgm & 1)) {
-          constexpr int NCH = X / C1;
-          const int jj = wt % NCH, G = wt / NCH;
-          float2 v[8][It<3, C1>::T / 2];
-          item_load<3, C1>(oFc + (G * 8) * PF + C1 * jj, PF, 0, v);
-          item_fht<3, C1>(v);
-          const int gb = G & (NR2 - 1);
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int o = oS + (G * 8 + r) * PS + HS + C1 * jj + ((r * gb) & 3);
-#pragma unroll
-            for (int tt = 0; tt < C1; ++tt) sm[o + tt] = col(v[r], It<3, C1>::O + tt);
-          }
-        }
-        named_sync(2, NW);                               // S1 complete
-        if (j >= ja && !(dbgm & 2)) {
-          constexpr int NCH2 = X / C2;
-          const int jj = wt % NCH2, c = wt / NCH2;
-          const int ubase = j * X + C2 * jj;
-          const bool need2 = (ubase + C2 > N - b * (c * NR2 + NR2)) && (ubase < W - c * NR2 * b);
-          if (need2) {
-            float2 v[NR2][It<R2, C2>::T / 2];
-            item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
-            item_fht<R2, C2>(v);
-#pragma unroll
-            for (int r = 0; r < NR2; ++r) {
-              const int cf = c * NR2 + r;
-              const int ulo = N - b * (cf + 1);
-              const int uhi = W - cf * b;
-              float* o = dstR + (long long)cf * NB * g.WR + (cf * b - N + NB);
-              const int res = (r * b) & 3;
-              if (ubase >= ulo && ubase + C2 <= uhi) {
-                if (res == 0) {
-#pragma unroll
-                  for (int tt = 0; tt < C2; tt += 4)
-                    st_ef4(o + ubase + tt, col(v[r], O2 + tt), col(v[r], O2 + tt + 1), col(v[r], O2 + tt + 2),
-                           col(v[r], O2 + tt + 3), pol_ef);
-                } else if (res == 2) {
-#pragma unroll
-                  for (int tt = 0; tt < C2; tt += 2)
-                    st_ef2(o + ubase + tt, col(v[r], O2 + tt), col(v[r], O2 + tt + 1), pol_ef);
-                } else {
-#pragma unroll
-                  for (int tt = 0; tt < C2; ++tt) st_ef(o + ubase + tt, col(v[r], O2 + tt), pol_ef);
-                }
-              } else if (ubase + C2 > ulo && ubase < uhi) {
-#pragma unroll
-                for (int tt = 0; tt < C2; ++tt) {
-                  const int u = ubase + tt;
-                  if (u >= ulo && u < uhi) st_ef(o + u, col(v[r], O2 + tt), pol_ef);
-                }
-              }
-            }
-          }
-        }
-        named_sync(2, NW);                               // step 2's S1 reads done
-        {
-          float4 tq[HT::NKH];
-#pragma unroll
-          for (int kk = 0; kk < HT::NKH; ++kk)
-            if (hoff[kk] != 0xffffu) tq[kk] = ld4(oS + (int)hoff[kk] + X);
-#pragma unroll
-          for (int kk = 0; kk < HT::NKH; ++kk)
-            if (hoff[kk] != 0xffffu) st4(oS + (int)hoff[kk], tq[kk]);
-        }
-      }
-      // the item's last F tile is done
-      if (jb > j1) mbar_arrive(bar_ffree((nfw - 1) & 1));
-    }
-    (void)nraw0;
-    (void)nf0;
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  if (tid < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(*s_tmem), "r"(g.tmem_cols)
-                 : "memory");
-}
-
-// ===========================================================================
-// Dual-pipeline sweep (fast path with the IIR at H = 64, X = 64: N = 2048, 4096).
-// One CTA per SM, 12 warps = two independent sweep pipelines ("halves"), each with
-//   2 recursion warps (thread = one linogram row of the tile: both recursions of the
-//     whole 64-sample row in ONE packed 64-step loop, .x causal left to right from the
-//     exact carry, .y anticausal right to left from zero state at the tile's right
-//     edge -- no chunk scan and no in-tile fix-up; P(t) parked in tensor memory,
-//     the anticausal carry added D tiles later from the plan table GA64)
-//   4 FHT warps (thread = one register item per step: step 1, step 2, R stores).
-// Warpgroup 0 (warps 0-3) holds the recursion warps of both halves (232 registers via
-// setmaxnreg), warpgroups 1 and 2 the FHT warps of half 0 and half 1 (136 registers),
-// so every SM sub-partition (warp % 4) runs one recursion and two FHT warps.  Each half
-// has its own work items, buffers RAW[2] / F[2] / S1 / ring, mbarriers rawfull[2]
-// (TMA), fready[2] (recursion -> FHT), ffree[2] (FHT -> recursion) and named barriers.
-// The FP32 pipe (128 lanes/clk/SM, FFMA2 issuing at half rate) bounds this kernel:
-// the thread-per-row recursion needs ~16 FP32 lane-ops per sample vs ~24 with the
-// 32-sample chunk scan and fix-up of k_sweep_a.
-// ===========================================================================
-template <bool BETA>
-__global__ void __launch_bounds__(384, 1)
-    k_sweep_dual(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k, int slices,
-                 int f0, int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
-                 const __grid_constant__ CUtensorMap tmapF) {
-  constexpr int H = 64, X = 64;
-  constexpr int R2 = 3, C1 = 4, C2 = 4;
-  constexpr int O2 = It<R2, C2>::O;
-  constexpr int NR2 = 1 << R2;
-  constexpr int HF = 8;
-  constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);
-  constexpr int PF = pitch4(HF + X + 4);
-  constexpr int PS = pitch4(HS + X + 4);
-  constexpr int NF = 128;                                // FHT threads per half
-  using HT = HaloTab<H, HS, O2, PS, NF>;
-  const int D = g.D;
-  // per-half shared-memory layout (floats)
-  const int oRaw = 0, oF = 2 * H * PF, oS = oF + 2 * H * PF, oRing = oS + H * PS;
-  const int oBar = (oRing + (D + 2) * H * 3 + 3) & ~1;   // 6 mbarriers (12 floats) + 2 item slots
-  const int HALF = (oBar + 16 + 31) & ~31;
-
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const bool rec = warp < 4;
-  const int half = rec ? (warp >> 1) : (warp < 8 ? 0 : 1);
-  const int rw = warp & 1;                               // recursion warp index in the half
-  const int ft = rec ? 0 : tid - 128 - 128 * half;       // FHT thread index in the half
-  const int base = half * ((HALF + 0));
-  const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
-  const int barI = 1 + 3 * half, barF = 2 + 3 * half, barH = 3 + 3 * half;
-  auto bar_raw = [&](int i) { return smem_u32(base + oBar + 2 * i); };
-  auto bar_fready = [&](int i) { return smem_u32(base + oBar + 4 + 2 * i); };
-  auto bar_ffree = [&](int i) { return smem_u32(base + oBar + 8 + 2 * i); };
-  int* s_item = reinterpret_cast<int*>(sm + base + oBar + 12);     // [2]
-  unsigned* s_tmem = reinterpret_cast<unsigned*>(sm + oBar + 14);   // in half 0's area
-  if (tid == 0) {
-    for (int hh = 0; hh < 2; ++hh)
-      for (int i = 0; i < 2; ++i) {
-        mbar_init(smem_u32(hh * HALF + oBar + 2 * i), 1);
-        mbar_init(smem_u32(hh * HALF + oBar + 4 + 2 * i), 64);
-        mbar_init(smem_u32(hh * HALF + oBar + 8 + 2 * i), NF);
-      }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(oBar + 14)),
-                 "r"(g.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const unsigned tbase = *s_tmem + ((unsigned)(32 * (warp & 3)) << 16);   // this warp's TMEM lanes
-  const int N = g.N, W = g.W, NB = g.NB, nt = g.nt;
-  const long long nsf = (long long)slices * nf;
-  const long long nitems = nsf * NB * nseg;
-  const unsigned long long pol_ef = policy_evict_first();
-  const int r = rw * 32 + lane;                          // recursion thread: its row
-  unsigned hoff[HT::NKH];
-#pragma unroll
-  for (int kk = 0; kk < HT::NKH; ++kk) hoff[kk] = rec ? 0xffffu : kHaloTab<H, HS, O2, PS, NF>.v[kk * NF + ft];
-  unsigned nraw = 0, nfw = 0;
-  const bool leader = rec && rw == 0 && lane == 0;       // issues TMA and dequeues
-  const int bsm = base;                                  // shared-memory base of this half
-
-  for (int iter = 0;; ++iter) {
-    if (leader) s_item[iter & 1] = atomicAdd(counter, 1);
-    named_sync(barH, 64 + NF);
-    const long long item = s_item[iter & 1];
-    if (item >= nitems) break;
-    const int seg = (int)(item % nseg);
-    const long long it2 = item / nseg;
-    const int b = NB - 1 - (int)(it2 / nsf);
-    const long long sfi = it2 - (long long)(NB - 1 - b) * nsf;
-    const long long s = sfi / nf;
-    const int fi = (int)(sfi - s * nf);
-    const int f = f0 + fi;
-    const int j0 = (N - (b + 1) * H + 1) / X;
-    const int seglen = (nt - j0 + nseg - 1) / nseg;
-    const int ja = j0 + seg * seglen, jb = min(nt, ja + seglen);
-    if (ja >= jb) continue;
-    const int j1 = (seg == 0) ? j0 : ja - 1;
-    const int jst = max(0, j1 - D);
-    const int tend = jb + D;
-    const int tlast = min(nt, tend);
-    const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
-
-    if (rec) {
-      // ========================= recursion warps =========================
-      auto land = [&](int jt, unsigned n) {
-        if (leader && !(dbgm & 8)) {
-          fence_proxy_async();
-          mbar_expect_tx(bar_raw(n & 1), H * PF * 4);
-          tma_load_2d(smem_u32(bsm + oRaw + (n & 1) * H * PF), &tmapF, jt * X - 8, trow, bar_raw(n & 1));
-        }
-      };
-      constexpr int PFD = 4;
-      auto prefetch = [&](int jt) {
-        if (leader && jt < nt && !(dbgm & 8)) tma_prefetch_2d(&tmapF, jt * X - 8, trow);
-      };
-      land(jst, nraw);
-      if (jst + 1 < tlast) land(jst + 1, nraw + 1);
-      for (int i = 2; i <= PFD + 1; ++i) prefetch(jst + i);
-      float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;
-      const int ringr = bsm + oRing + r * 3;             // this row's ring entries (private)
-      // The back step of iteration t finalises tile j = t - (D+1), one tile later than
-      // strictly needed, so that it depends only on agg[] of earlier iterations and its
-      // instructions interleave with the front's recursion chain (one fused loop).
-      const int NS = D + 2;                              // ring / TMEM slots
-      int slot_t = 0;                                    // slot of tile t: (t - jst) mod NS
-      auto body = [&](auto fF, auto fB, int t) {
-        constexpr bool DF = decltype(fF)::value, DB = decltype(fB)::value;
-        const int sj = (slot_t + 1 == NS) ? 0 : slot_t + 1;   // slot of j = t - NS + 1
-        float2 t0 = make_float2(0.f, 0.f), t1 = t0, t2 = t0;
-        int rowF = 0;
-        unsigned nb = 0;
-        if (DB) {
-          // T_j = sum_{i=1..D} (A^X)^(i-1) agg[j+i]: tiles t-1 down to t-D (Horner)
-          float tm[3];
-          int sl = (slot_t == 0) ? NS - 1 : slot_t - 1;
-          tm[0] = sm[ringr + sl * H * 3];
-          tm[1] = sm[ringr + sl * H * 3 + 1];
-          tm[2] = sm[ringr + sl * H * 3 + 2];
-          for (int i = D - 1; i >= 1; --i) {
-            sl = (sl == 0) ? NS - 1 : sl - 1;
-            float acc[3] = {sm[ringr + sl * H * 3], sm[ringr + sl * H * 3 + 1], sm[ringr + sl * H * 3 + 2]};
-            mv1(k.MX, tm, acc);
-            tm[0] = acc[0];
-            tm[1] = acc[1];
-            tm[2] = acc[2];
-          }
-          t0 = make_float2(tm[0], tm[0]);
-          t1 = make_float2(tm[1], tm[1]);
-          t2 = make_float2(tm[2], tm[2]);
-          nb = nfw++;
-          if (nb >= 2) mbar_wait(bar_ffree(nb & 1), ((nb >> 1) - 1) & 1);
-          rowF = bsm + oF + (nb & 1) * H * PF + r * PF + HF;
-          tmem_wait_st();
-        }
-        unsigned n = 0;
-        int row = 0;
-        if (DF) {
-          n = nraw++;
-          if (!(dbgm & 8)) mbar_wait(bar_raw(n & 1), (n >> 1) & 1);
-          row = bsm + oRaw + (n & 1) * H * PF + r * PF + HF;   // sample 0 of the tile row
-        }
-        // front: one packed 64-step loop (.x causal at k, .y anticausal at 63 - k);
-        // steps 0..31 kept (ya), from step 32 on P(t)[k] and P(t)[63-k] complete and
-        // go to tensor memory in groups of 8 columns.  Back: P(j) + carry response.
-        float2 ya[32];
-        float Pb[32];
-        float c0v = 0.f, c1v = 0.f, c2v = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
-        float pl = 0.f, pr = 0.f;
-        float2 dprev = make_float2(0.f, 0.f);
-        float2 y1 = make_float2(cin0, 0.f), y2 = make_float2(cin1, 0.f), y3 = make_float2(cin2, 0.f);
-        float phi[8], plo[8];
-        if (DF) {
-          const float4 vl = ld4(row - 4);
-          const float4 vr = ld4(row + 64);
-          pl = vl.w;
-          pr = vr.x;
-          dprev = make_float2(vl.w - vl.z, vr.x - vr.y);
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          if (DB && (q & 7) == 0) tmem_ld32(tbase + 64u * sj + 32u * (q >> 3), Pb);
-          if (DF) {
-            const float4 a4 = ld4(row + 4 * q);
-            const float4 b4 = ld4(row + 60 - 4 * q);
-            const float xa[4] = {a4.x, a4.y, a4.z, a4.w};
-            const float xb[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int kk = 4 * q + u;
-              const float xi = xa[u], xim1 = (u == 0) ? pl : xa[u - 1];
-              const float xr = xb[3 - u], xrp1 = (u == 0) ? pr : xb[4 - u];
-              float2 d;
-              d.x = xi - xim1;
-              d.y = xr - xrp1;
-              float2 uu = __fmul2_rn(k.c1, dprev);
-              uu = __ffma2_rn(k.c0, d, uu);
-              if (BETA) {
-                uu.x = fmaf(k.beta.x, xi, uu.x);
-                uu.y = fmaf(k.beta.x, xr, uu.y);
-              }
-              float2 v = __ffma2_rn(k.na3, y3, uu);
-              v = __ffma2_rn(k.na2, y2, v);
-              v = __ffma2_rn(k.na1, y1, v);
-              y3 = y2;
-              y2 = y1;
-              y1 = v;
-              dprev = d;
-              if (kk < 32) {
-                ya[kk] = v;
-              } else {
-                phi[kk & 7] = v.x + ya[63 - kk].y;         // P(t)[kk]
-                plo[7 - (kk & 7)] = ya[63 - kk].x + v.y;   // P(t)[63 - kk]
-                if ((kk & 7) == 7) {
-                  const int k0 = kk - 7;
-                  tmem_st8(tbase + 64u * slot_t + (unsigned)k0, phi);
-                  tmem_st8(tbase + 64u * slot_t + (unsigned)(56 - k0), plo);
-                }
-              }
-              if (kk == 61) { c2v = v.x; g2 = v.y; }
-              if (kk == 62) { c1v = v.x; g1 = v.y; }
-              if (kk == 63) { c0v = v.x; g0 = v.y; }
-            }
-            pl = xa[3];
-            pr = xb[0];
-          }
-          if (DB) {
-            // samples 4q .. 4q+3 of F(j): pairs 2q, 2q+1 of the table
-            const int qq = q & 7;
-            float2 aa = make_float2(Pb[4 * qq], Pb[4 * qq + 1]);
-            float2 cc2 = make_float2(Pb[4 * qq + 2], Pb[4 * qq + 3]);
-            aa = __ffma2_rn(k.GA64[2 * q][0], t0, aa);
-            aa = __ffma2_rn(k.GA64[2 * q][1], t1, aa);
-            aa = __ffma2_rn(k.GA64[2 * q][2], t2, aa);
-            cc2 = __ffma2_rn(k.GA64[2 * q + 1][0], t0, cc2);
-            cc2 = __ffma2_rn(k.GA64[2 * q + 1][1], t1, cc2);
-            cc2 = __ffma2_rn(k.GA64[2 * q + 1][2], t2, cc2);
-            st4(rowF + 4 * q, make_float4(aa.x, aa.y, cc2.x, cc2.y));
-          }
-        }
-        if (DF) {
-          cin0 = c0v;
-          cin1 = c1v;
-          cin2 = c2v;
-          sm[ringr + slot_t * H * 3] = g0;                // agg[t]: zero-state anticausal
-          sm[ringr + slot_t * H * 3 + 1] = g1;            // state at the tile's left edge
-          sm[ringr + slot_t * H * 3 + 2] = g2;
-          named_sync(barI, 64);                           // RAW[n & 1] read by every row
-          if (t + 2 < tlast) land(t + 2, n + 2);
-          prefetch(t + 2 + PFD);
-        } else {
-          sm[ringr + slot_t * H * 3] = 0.f;
-          sm[ringr + slot_t * H * 3 + 1] = 0.f;
-          sm[ringr + slot_t * H * 3 + 2] = 0.f;
-        }
-        if (DB) mbar_arrive(bar_fready(nb & 1));
-      };
-      using T_ = std::true_type;
-      using F_ = std::false_type;
-      for (int t = jst; t < jb + NS - 1; ++t, slot_t = (slot_t == NS - 1) ? 0 : slot_t + 1) {
-        const bool front = t < tlast;
-        const bool back = t - (NS - 1) >= j1;
-        if (front && back) body(T_{}, T_{}, t);
-        else if (front) body(T_{}, F_{}, t);
-        else if (back) body(F_{}, T_{}, t);
-        else body(F_{}, F_{}, t);
-      }
-    } else {
-      // ============================ FHT warps ============================
-      for (int e = ft; e < H * (HS / 4); e += NF) {
-        const int rr = e / (HS / 4), qd = e - rr * (HS / 4);
-        st4(bsm + oS + rr * PS + 4 * qd, make_float4(0.f, 0.f, 0.f, 0.f));
-      }
-      float* dstR = Rout + (((s * 4 + f) * (long long)H) * NB + b) * g.WR;
-      for (int j = j1; j < jb; ++j) {
-        const unsigned n = nfw++;
-        mbar_wait(bar_fready(n & 1), (n >> 1) & 1);
-        const int oFc = bsm + oF + (n & 1) * H * PF, oFp = bsm + oF + ((n + 1) & 1) * H * PF;
-        for (int e = ft; e < 2 * H; e += NF) {
-          const int rr = e >> 1, qd = e & 1;
-          const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oFp + rr * PF + X + 4 * qd);
-          st4(oFc + rr * PF + 4 * qd, h);
-        }
-        named_sync(barF, NF);
-        if (j > j1) mbar_arrive(bar_ffree((n + 1) & 1));
-        if (!(dbgm & 1)) {
-          {
-            constexpr int NCH = X / C1;
-            const int itm = ft;
-            const int jj = itm % NCH, G = itm / NCH;
-            float2 v[8][It<3, C1>::T / 2];
-            item_load<3, C1>(oFc + (G * 8) * PF + C1 * jj, PF, 0, v);
-            item_fht<3, C1>(v);
-            const int gb = G & (NR2 - 1);
-#pragma unroll
-            for (int rr = 0; rr < 8; ++rr) {
-              const int o = bsm + oS + (G * 8 + rr) * PS + HS + C1 * jj + ((rr * gb) & 3);
-#pragma unroll
-              for (int tt = 0; tt < C1; ++tt) sm[o + tt] = col(v[rr], It<3, C1>::O + tt);
-            }
-          }
-        }
-        named_sync(barF, NF);
-        if (j >= ja && !(dbgm & 2)) {
-          {
-            constexpr int NCH2 = X / C2;
-            const int itm = ft;
-            const int jj = itm % NCH2, c = itm / NCH2;
-            const int ubase = j * X + C2 * jj;
-            const bool need2 = (ubase + C2 > N - b * (c * NR2 + NR2)) && (ubase < W - c * NR2 * b);
-            if (need2) {
-              float2 v[NR2][It<R2, C2>::T / 2];
-              item_load<R2, C2>(bsm + oS + c * PS + HS + C2 * jj - O2, 8 * PS, c, v);
-              item_fht<R2, C2>(v);
-#pragma unroll
-              for (int rr = 0; rr < NR2; ++rr) {
-                const int cf = c * NR2 + rr;
-                const int ulo = N - b * (cf + 1);
-                const int uhi = W - cf * b;
-                float* o = dstR + (long long)cf * NB * g.WR + (cf * b - N + NB);
-                const int res = (rr * b) & 3;
-                if (ubase >= ulo && ubase + C2 <= uhi) {
-                  if (res == 0) {
-                    st_ef4(o + ubase, col(v[rr], O2), col(v[rr], O2 + 1), col(v[rr], O2 + 2), col(v[rr], O2 + 3),
-                           pol_ef);
-                  } else if (res == 2) {
-                    st_ef2(o + ubase, col(v[rr], O2), col(v[rr], O2 + 1), pol_ef);
-                    st_ef2(o + ubase + 2, col(v[rr], O2 + 2), col(v[rr], O2 + 3), pol_ef);
-                  } else {
-#pragma unroll
-                    for (int tt = 0; tt < C2; ++tt) st_ef(o + ubase + tt, col(v[rr], O2 + tt), pol_ef);
-                  }
-                } else if (ubase + C2 > ulo && ubase < uhi) {
-#pragma unroll
-                  for (int tt = 0; tt < C2; ++tt) {
-                    const int u = ubase + tt;
-                    if (u >= ulo && u < uhi) st_ef(o + u, col(v[rr], O2 + tt), pol_ef);
-                  }
-                }
-              }
-            }
-          }
-        }
-        named_sync(barF, NF);
-        {
-          float4 tq[HT::NKH];
-#pragma unroll
-          for (int kk = 0; kk < HT::NKH; ++kk)
-            if (hoff[kk] != 0xffffu) tq[kk] = ld4(bsm + oS + (int)hoff[kk] + X);
-#pragma unroll
-          for (int kk = 0; kk < HT::NKH; ++kk)
-            if (hoff[kk] != 0xffffu) st4(bsm + oS + (int)hoff[kk], tq[kk]);
-        }
-      }
-      if (jb > j1) mbar_arrive(bar_ffree((nfw - 1) & 1));
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(*s_tmem), "r"(g.tmem_cols)
-                 : "memory");
-}
-
-// ===========================================================================
 // Pass B, one family pair (Eq.22): CTA item = (slice, pass-A channel ch, x-tile).
 // Family 2p (q = 0) at x0, family 2p+1 (q = 1) at the mirrored tile N - x0 - XB.
 // Input rows b of G_ch[b][v] = R_A[b][ch][v - ch*b] (compact layout; the
@@ -1886,83 +1100,6 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
   return cudaGetLastError();
 }
 
-size_t sweep_ws_smem(const SweepGeom& g) {
-  const int H = g.H, X = g.X;
-  const int R2 = (H == 64) ? 3 : 2;
-  const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : 4 + 4 * ((7 * 3) / 4);
-  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
-  const size_t fl = (size_t)4 * H * PF + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 16;
-  return fl * sizeof(float);
-}
-
-template <int H, int X, bool BETA>
-static cudaError_t launch_ws_t(const float* lin, float* R, int slices, int f0, int nf, long long stride,
-                               const SweepGeom& g, const SweepIir& k, int* counter, cudaStream_t st) {
-  auto kern = k_sweep_ws<H, X, BETA>;
-  const size_t smem = sweep_ws_smem(g);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, smem_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  int per = std::min<int>(2, (int)(smem_sm / (smem + 1024)));
-  per = std::min(per, 512 / g.tmem_cols);
-  if (g.ctas_a > 0 && g.ctas_a < per) per = g.ctas_a;
-  if (per < 1) per = 1;
-  const long long sweeps = (long long)slices * nf * g.NB;
-  const long long slots = (long long)sms * per * 3 / 2;   // a WS CTA ~ 1.5 single-role CTAs of work
-  int nseg = (int)std::min<long long>(8, std::max<long long>(1, (17 * slots + 10 * sweeps - 1) / (10 * sweeps)));
-  if (g.nseg > 0) nseg = g.nseg;
-  const long long nitems = sweeps * nseg;
-  const long long grid = std::min<long long>(nitems, (long long)sms * per);
-  CUtensorMap tF;
-  e = make_lin_map(&tF, lin, slices, g, pitch4(8 + X + 4), H);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, 2 * H * X / 32, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, nseg, counter, tF);
-  return cudaGetLastError();
-}
-
-size_t sweep_dual_smem(const SweepGeom& g) {
-  const int H = 64, X = 64, HS = 8 + 4 * ((7 * 7) / 4);
-  const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
-  const int oRing = 4 * H * PF + H * PS;
-  const int oBar = (oRing + (g.D + 2) * H * 3 + 3) & ~1;
-  const int HALF = (oBar + 16 + 31) & ~31;
-  return (size_t)2 * HALF * sizeof(float);
-}
-
-template <bool BETA>
-static cudaError_t launch_dual_t(const float* lin, float* R, int slices, int f0, int nf, long long stride,
-                                 SweepGeom g, const SweepIir& k, int* counter, cudaStream_t st) {
-  auto kern = k_sweep_dual<BETA>;
-  const size_t smem = sweep_dual_smem(g);
-  int cols = 32;
-  while (cols < 64 * (g.D + 2)) cols *= 2;
-  if (cols > 512) return cudaErrorInvalidValue;
-  g.tmem_cols = cols;                                    // 64 columns per slot and lane (D+2 slots)
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long sweeps = (long long)slices * nf * g.NB;
-  const long long slots = (long long)sms * 2 * 3 / 2;    // two pipelines per CTA
-  int nseg = (int)std::min<long long>(8, std::max<long long>(1, (17 * slots + 10 * sweeps - 1) / (10 * sweeps)));
-  if (g.nseg > 0) nseg = g.nseg;
-  const long long nitems = sweeps * nseg;
-  const long long grid = std::min<long long>((nitems + 1) / 2, (long long)sms);
-  CUtensorMap tF;
-  e = make_lin_map(&tF, lin, slices, g, pitch4(8 + 64 + 4), 64);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, 384, smem, st>>>(lin, R, g, k, slices, f0, nf, stride, nseg, counter, tF);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int nf,
                            long long lin_slice_stride, const SweepGeom& g, const SweepIir& k,
                            bool iir, int* counter, cudaStream_t st, int* launches) {
@@ -1976,10 +1113,6 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
 #define FBP_SWEEP_CASE(HH, XX)                                                                     \
   if (g.H == HH) {                                                                                 \
     if (!iir) e = launch_a_t<HH, XX, false, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
-    else if (HH == 64 && g.ws == 2 && beta) e = launch_dual_t<true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
-    else if (HH == 64 && g.ws == 2) e = launch_dual_t<false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
-    else if (g.ws == 1 && beta) e = launch_ws_t<HH, XX, true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
-    else if (g.ws == 1) e = launch_ws_t<HH, XX, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
     else if (beta) e = launch_a_t<HH, XX, true, true>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
     else e = launch_a_t<HH, XX, true, false>(lin, R, slices, f0, nf, lin_slice_stride, g, k, counter, st); \
     if (launches) ++*launches;                                                                     \
