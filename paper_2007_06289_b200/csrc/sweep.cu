@@ -781,9 +781,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 // input buffer) and the pair epilogue mirrors, adds, weights and stores:
 //   PAIR 0:  img[ch*NB + r][x0 + i]  = w (B0[r][i] + B1[r][XB-1-i])
 //   PAIR 1:  img[x0 + i][ch*NB + r] += w (B2[r][i] + B3[r][XB-1-i])
-// For PAIR 1 the image rows are staged into shared memory by TMA while the FHT
-// steps run.  Pair 0 runs 3 CTAs per SM, pair 1 two; the next item's boxes land
-// while this one computes (double buffer).
+// PAIR 1 adds its tile by a TMA tensor reduce (cp.reduce.async.bulk.tensor .add,
+// performed in L2) from a staging tile behind the park; it runs after pair 0 in
+// stream order, so every image element is pair 0's value plus one fp32 add, as
+// before (bit-identical to a read-modify-write).  Both pairs run 3 CTAs per SM; the
+// next item's boxes land while this one computes (double buffer).
 // ===========================================================================
 // Pass-B item position (slice, channel, x tile).  Items are visited with the grid
 // stride; the stride is decomposed once and added with mixed-radix carries, so the
@@ -809,8 +811,19 @@ __device__ __forceinline__ PbPos pb_add(PbPos a, const PbPos& d, int nx, int H) 
   return a;
 }
 
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, unsigned src, int c0, int r0) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];\n"
+               ::"l"(reinterpret_cast<unsigned long long>(map)), "r"(src), "r"(c0), "r"(r0)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 template <int R1, int R2, int XB, int PAIR, bool DB>
-__global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
+__global__ void __launch_bounds__(256, DB ? 3 : 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
              long long nitems, const __grid_constant__ CUtensorMap tmapR,
              const __grid_constant__ CUtensorMap tmapI) {
@@ -827,21 +840,22 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
   constexpr int PI = pitch4(4 * NQF);
   constexpr int PS = pitch4(HS + XB + 4);
   constexpr int PK = PAIR == 0 ? XB + 4 : XB + 1;     // pair 1 reads park columns
-  constexpr int PG = NB;                              // image staging pitch (pair 1, TMA box)
-  // DB: two input (and staging) buffers, the next item's TMA boxes land while this
-  // item computes
+  // DB: two input buffers, the next item's TMA boxes land while this item computes
   constexpr int NBUF = DB ? 2 : 1;
-  constexpr int IN_SZ = 2 * NB * PI, G_SZ = PAIR == 1 ? XB * PG : 0;   // pair 0 stages no image
+  // pair 1: reduce staging [XB][NB] behind the park, 128-byte aligned, in the input buffer
+  constexpr int oStg = (2 * NB * PK + 31) / 32 * 32;
+  constexpr int IN_SZ = (PAIR == 1 && oStg + XB * NB > 2 * NB * PI) ? oStg + XB * NB : 2 * NB * PI;
   constexpr int oIn0 = 0;                             // [NBUF][2 fam][NB][PI]; park aliases it
   constexpr int oS = NBUF * IN_SZ;                    // [2 fam][NB][PS]
-  constexpr int oG0 = oS + 2 * NB * PS;               // [NBUF][XB][PG] image rows (pair 1)
   static_assert((HS + XB) % C1 == 0 && XB % C2 == 0, "pass-B item tiling");
   static_assert(2 * NB * PK <= 2 * NB * PI, "park must fit in the input buffer");
+  static_assert(PAIR == 0 || oStg + XB * NB <= IN_SZ, "reduce staging must fit in the input buffer");
+  static_assert((IN_SZ % 32) == 0, "input buffers 128-byte aligned");
   const int N = g.N, H = g.H;
   const int tid = threadIdx.x;
   const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
   const int nx = (N + XB - 1) / XB;
-  constexpr int oBar = oG0 + NBUF * G_SZ;             // NBUF mbarriers (8-byte aligned)
+  constexpr int oBar = oS + 2 * NB * PS;              // NBUF mbarriers (8-byte aligned)
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -850,8 +864,8 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
   unsigned ph = 0;
   // TMA fills of item tt into buffer bb (thread 0): both families' NB compact rows
   // of channel ch (3D box PI x NB x 1, columns j' = xs - HI + NB.., zero-filled
-  // outside the row), for pair 1 the XB image rows x0.. (2D box NB x XB); plus an
-  // L2 prefetch of the boxes of item tt + P*gridDim.x
+  // outside the row); plus an L2 prefetch of the boxes of item tt + P*gridDim.x.
+  // Pair 1: the buffer's previous reduce must have read its staging first.
   const int nsl = (int)(nitems / ((long long)nx * H));
   const PbPos step = pb_pos(gridDim.x, nx, H);
   const PbPos stepP = pb_pos((long long)g.P * gridDim.x, nx, H);
@@ -866,20 +880,19 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
           const int xs = (q == 0) ? x0p : (N - x0p - XB);
           tma_prefetch_3d(&tmapR, xs - HI + NB, 0, (pp.sl * 4 + 2 * PAIR + q) * H + pp.ch);
         }
-        if (PAIR == 1) tma_prefetch_2d(&tmapI, pp.ch * NB, pp.sl * N + x0p);
       }
     }
     const int sl2 = pt.sl, ch2 = pt.ch, x02 = pt.xi * XB;
+    if (PAIR == 1) bulk_wait_read_all();
     fence_proxy_async();
     const unsigned bar = smem_u32(oBar + 2 * bb);
-    mbar_expect_tx(bar, 2u * NB * PI * 4 + (PAIR == 1 ? (unsigned)XB * PG * 4 : 0u));
+    mbar_expect_tx(bar, 2u * NB * PI * 4);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int xs = (q == 0) ? x02 : (N - x02 - XB);
       tma_load_3d(smem_u32(oIn0 + bb * IN_SZ + q * NB * PI), &tmapR, xs - HI + NB, 0,
                   (sl2 * 4 + 2 * PAIR + q) * H + ch2, bar);
     }
-    if (PAIR == 1) tma_load_2d(smem_u32(oG0 + bb * G_SZ), &tmapI, ch2 * NB, sl2 * N + x02, bar);
   };
   PbPos cur = pb_pos(blockIdx.x, nx, H);
   issue(cur, 0);
@@ -888,11 +901,10 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
   for (; cur.sl < nsl; cur = pb_add(cur, step, nx, H)) {
     const int ch = cur.ch;
     const int x0 = cur.xi * XB;
-    const int oIn = oIn0 + bb * IN_SZ, oG = oG0 + bb * G_SZ;
+    const int oIn = oIn0 + bb * IN_SZ;
     if (DB) issue(pb_add(cur, step, nx, H), bb ^ 1);   // buffer freed by the previous item
     // ---- fills by TMA: both families' NB compact rows of channel ch (3D box
-    //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row),
-    //      and for pair 1 the XB image rows x0.. (columns ch*NB.., 2D box NB x XB) ----
+    //      PI x 1 x NB, columns j' = xs - HI + NB.., zero-filled outside the row) ----
     if (!(dbgm & 4)) mbar_wait(smem_u32(oBar + 2 * bb), (ph >> bb) & 1);
     ph ^= 1u << bb;
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
@@ -958,25 +970,29 @@ __global__ void __launch_bounds__(256, (PAIR == 0 && DB) ? 3 : 2)
         }
       }
     } else {
-      // lanes: 8 row-quads of one image row x 4 image rows per warp (coalesced 128 B rows)
+      // staging tile [XB image rows x0 + i][NB image columns ch*NB + r] (the TMA box):
+      // lanes = 8 row-quads of one image row x 4 image rows per warp
       constexpr int gq = NB / 4;
-      float* const outc = img + ((long long)cur.sl * N + x0) * N + ch * NB;   // image rows x0..
       for (int e = tid; e < XB * gq; e += NT) {
         const int i = e / gq, rq = e - i * gq;
-        if (x0 + i >= N) continue;
         const int rf = 4 * rq;
-        float4 o = ld4(oG + i * PG + rf);
-        o.x += scale * (sm[oIn + rf * PK + i] + sm[oIn + (NB + rf) * PK + XB - 1 - i]);
-        o.y += scale * (sm[oIn + (rf + 1) * PK + i] + sm[oIn + (NB + rf + 1) * PK + XB - 1 - i]);
-        o.z += scale * (sm[oIn + (rf + 2) * PK + i] + sm[oIn + (NB + rf + 2) * PK + XB - 1 - i]);
-        o.w += scale * (sm[oIn + (rf + 3) * PK + i] + sm[oIn + (NB + rf + 3) * PK + XB - 1 - i]);
-        *reinterpret_cast<float4*>(outc + i * N + rf) = o;
+        float4 o;
+        o.x = scale * (sm[oIn + rf * PK + i] + sm[oIn + (NB + rf) * PK + XB - 1 - i]);
+        o.y = scale * (sm[oIn + (rf + 1) * PK + i] + sm[oIn + (NB + rf + 1) * PK + XB - 1 - i]);
+        o.z = scale * (sm[oIn + (rf + 2) * PK + i] + sm[oIn + (NB + rf + 2) * PK + XB - 1 - i]);
+        o.w = scale * (sm[oIn + (rf + 3) * PK + i] + sm[oIn + (NB + rf + 3) * PK + XB - 1 - i]);
+        st4(oIn + oStg + i * NB + rf, o);
       }
+      fence_proxy_async();                             // staging -> async proxy (each writer)
     }
     __syncthreads();                                   // park / staging reused by the next item
+    // pair 1: image[x0 + i][ch*NB + r] += staging (TMA reduce in L2; clipped at row N)
+    if (PAIR == 1 && tid == 0 && !(dbgm & 2))
+      tma_reduce_add_2d(&tmapI, smem_u32(oIn + oStg), ch * NB, cur.sl * N + x0);
     if (!DB) issue(pb_add(cur, step, nx, H), 0);
     if (DB) bb ^= 1;
   }
+  if (PAIR == 1 && tid == 0) bulk_wait_all();          // reduces complete before exit
 }
 
 // ---------------------------------------------------------------- host side
@@ -1003,7 +1019,11 @@ size_t pair_b_smem(const SweepGeom& g, int pair) {
   const int RPT = 256 / (2 * NB), NQF = ((HI + XB) / 4 + RPT - 1) / RPT * RPT;
   const int PI = pitch4(4 * NQF), PS = pitch4(HS + XB + 4), PG = NB;
   const size_t nbuf = db ? 2 : 1;
-  return (nbuf * 2 * NB * PI + (size_t)2 * NB * PS + (pair == 1 ? nbuf * XB * PG : 0) + 4) * sizeof(float);
+  (void)PG;
+  const int PK = pair == 0 ? XB + 4 : XB + 1;
+  const int oStg = (2 * NB * PK + 31) / 32 * 32;
+  const size_t in_sz = (pair == 1 && oStg + XB * NB > 2 * NB * PI) ? (size_t)oStg + XB * NB : (size_t)2 * NB * PI;
+  return (nbuf * in_sz + (size_t)2 * NB * PS + 4) * sizeof(float);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
