@@ -170,7 +170,11 @@ size_t fwd_workspace_floats(const Geometry& g) { return (size_t)4 * g.NB * g.H *
 // (H - 1, resp. NB - 1 columns) is a small overhead, narrow enough for >= 2 CTAs/SM
 static int fwd_tile(int rows, int dflt, const char* env) {
   int x = dflt;                                     // measured best at N = 2048 (r01)
-  if (const char* ev = std::getenv(env)) x = std::max(32, std::atoi(ev) / 32 * 32);
+#if FBP_DEV_MASK
+  if (const char* ev = std::getenv(env)) x = std::max(32, std::atoi(ev) / 32 * 32);   // developer builds only
+#else
+  (void)env;
+#endif
   while (x > 32 && (size_t)2 * rows * (x + rows + 1) * sizeof(float) > (size_t)227 * 1024) x -= 32;
   return x;
 }

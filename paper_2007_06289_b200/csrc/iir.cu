@@ -50,8 +50,10 @@ __device__ __forceinline__ void row_to_smem(const float* src, float* row_s, int 
 
 }  // namespace
 
-template <int QM, int MC, int L, bool BETA>
-__global__ void __launch_bounds__(512) k_iir(const float* in, float* out, int W,
+// MAXT: launch bound (threads = W / L): 256 up to W = 8192 (registers for the
+// order-8 chunk without spills), 512 for N = 8192
+template <int QM, int MC, int L, bool BETA, int MAXT>
+__global__ void __launch_bounds__(MAXT) k_iir(const float* in, float* out, int W,
                                              const float* __restrict__ lane_mats, IirParams p) {
   extern __shared__ float sm[];
   float* row_s = sm;                                   // W * 36/32 floats (padded)
@@ -279,7 +281,8 @@ static cudaError_t launch_L(const float* in, float* out, long long rows, const G
   const size_t smem = ((size_t)(g.W / 32 + 1) * 36 + 64 + 2 * 16 * kMaxOrder + 32 * QM * QM + 16) * sizeof(float);
   (void)nwarps;
   const bool beta = p.beta != 0.0f;
-  auto k = beta ? k_iir<QM, MC, L, true> : k_iir<QM, MC, L, false>;
+  auto k = (threads <= 256) ? (beta ? k_iir<QM, MC, L, true, 256> : k_iir<QM, MC, L, false, 256>)
+                            : (beta ? k_iir<QM, MC, L, true, 512> : k_iir<QM, MC, L, false, 512>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   for (long long r0 = 0; r0 < rows; r0 += 2147483647LL) {

@@ -93,3 +93,13 @@ def test_python_plan_raises_loudly_without_device():
     from paper_2007_06289_b200 import Plan, FbpError
     with pytest.raises(FbpError):
         Plan(64, [0.12, -0.23, 0.10], [-1.02, 0.0017, 0.0947])
+
+
+def test_product_build_reads_no_tuning_environment(L):
+    """Developer knobs (FBP_XB, FBP_TAIL, FBP_DBG, ...) exist only in -DFBP_DEV_MASK=1
+    builds: the product library contains none of their names."""
+    from paper_2007_06289_b200 import fbp
+    data = open(fbp._LIB_PATH, "rb").read()
+    for name in (b"FBP_XB", b"FBP_TAIL", b"FBP_DBG", b"FBP_PREFETCH", b"FBP_SWEEP_CTAS", b"FBP_SWEEP_SEG",
+                 b"FBP_FXA", b"FBP_FXB", b"FBP_VERBOSE"):
+        assert name not in data, name
