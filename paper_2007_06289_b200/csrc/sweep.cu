@@ -353,6 +353,34 @@ struct HaloTab {
 template <int H, int HS, int O2, int PS, int NT>
 __device__ constexpr HaloTab<H, HS, O2, PS, NT> kHaloTab{};
 
+// The same plan per step-1 row group G (S1 rows 8G .. 8G+7, written by the step-1
+// items of group G): the group's own threads copy its quads, so no CTA barrier is
+// needed between this copy and the group's next step 1.
+template <int H, int HS, int O2, int PS>
+struct HaloTabG {
+  static constexpr int MAXQ = (HS + 4) / 4;
+  static constexpr int NG = H / 8;
+  static constexpr int CAP = 8 * MAXQ;
+  unsigned short cnt[NG];
+  unsigned short v[NG][CAP];
+  constexpr HaloTabG() : cnt(), v() {
+    for (int G = 0; G < NG; ++G) {
+      int n = 0;
+      for (int r = 0; r < 8; ++r) {
+        const int rr = 8 * G + r;
+        const int cb = (rr & 7) * (rr >> 3);
+        int nq = (O2 + (cb & ~3)) / 4 + 1;
+        if (nq > MAXQ) nq = MAXQ;
+        for (int qd = 0; qd < nq; ++qd) v[G][n++] = (unsigned short)(rr * PS + HS - 4 * qd);
+      }
+      cnt[G] = (unsigned short)n;
+      for (; n < CAP; ++n) v[G][n] = 0xffff;
+    }
+  }
+};
+template <int H, int HS, int O2, int PS>
+__device__ constexpr HaloTabG<H, HS, O2, PS> kHaloTabG{};
+
 // ---- tensor memory (tcgen05): one 32-column slot of a thread's own lane ----
 __device__ __forceinline__ void tmem_st32(unsigned taddr, const float (&v)[32]) {
   asm volatile(
@@ -401,10 +429,6 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   const int tid = threadIdx.x;
   const int D = IIR ? g.D : 0;
   const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
-  using HT = HaloTab<H, HS, O2, PS, NT>;
-  unsigned hoff[HT::NKH];                                // this thread's S1 halo quads
-#pragma unroll
-  for (int kk = 0; kk < HT::NKH; ++kk) hoff[kk] = kHaloTab<H, HS, O2, PS, NT>.v[kk * NT + tid];
   // 1 mbarrier (F landing), the work item, the TMEM base address
   const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
   int* s_item = reinterpret_cast<int*>(sm + oBar + 2);
@@ -612,7 +636,9 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           sm[o + 1] = 0.f;
           sm[o + 2] = 0.f;
         }
-        __syncthreads();                                 // raw tile read, ring written
+        // every read of a row's raw data, and its ring entries, stay inside the row's
+        // warp (row r is chunks of threads in one warp; its F and halo writes too)
+        __syncwarp();
         if (back && !(dbgm & 64)) {
           // ---- back: F(j) = P(j) + anticausal homogeneous response of the carry ----
           // T_j = sum_{i=1..D} (A^X)^(i-1) agg[j+i] at tile j's right edge (Horner)
@@ -667,15 +693,15 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       } else {
         tma_wait();                                      // raw tile j = F(j) landed
       }
-      if (back) {
-        // halo: F(j-1)'s last HF columns (zero at the first back tile)
-        for (int e = tid; e < 2 * H; e += NT) {
-          const int r = e >> 1, qd = e & 1;
-          const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + r * HF + 4 * qd);
-          st4(oF + r * PF + 4 * qd, h);
-        }
+      if (back && iq < 2) {
+        // halo: F(j-1)'s last HF columns (zero at the first back tile), written by the
+        // row's own chunk threads 0 and 1
+        const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + ir * HF + 4 * iq);
+        st4(oF + ir * PF + 4 * iq, h);
       }
-      __syncthreads();                                   // F(j) complete
+      // F(j) rows 8G .. 8G+7 are complete: they were written by the same threads that
+      // run step 1 on them (row group G = the IIR threads of rows 8G..8G+7)
+      __syncwarp();
       if (back && !(dbgm & 1)) {
         // ---- FHT step 1 (levels 1-3): F -> S1 ----
         constexpr int NCH = X / C1;
@@ -690,13 +716,10 @@ __global__ void __launch_bounds__(H * X / 32, 3)
 #pragma unroll
           for (int tt = 0; tt < C1; ++tt) sm[o + tt] = col(v[r], It<3, C1>::O + tt);
         }
-        // stash this tile's last HF filtered columns (halo of the next tile)
-        for (int e = tid; e < 2 * H; e += NT) {
-          const int r = e >> 1, qd = e & 1;
-          st4(oStash + r * HF + 4 * qd, ld4(oF + r * PF + X + 4 * qd));
-        }
       }
-      __syncthreads();
+      // stash this tile's last HF filtered columns (halo of the next tile), row owners
+      if (back && iq < 2) st4(oStash + ir * HF + 4 * iq, ld4(oF + ir * PF + X + 4 * iq));
+      __syncthreads();                                   // F read by all (landing); S1 complete (step 2)
       // F is free: land the next raw tile
       if (IIR) {
         if (t + 1 < nt && t + 1 < tend) land(t + 1);
@@ -755,13 +778,16 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       // ---- S1 halo for the next tile: row (b', c) of step 2 reads virtual columns
       //      >= HS - O2 - c*b' only, so copy just those quads (+ the shift quad) ----
       if (back) {
-        float4 tq[HT::NKH];
-#pragma unroll
-        for (int kk = 0; kk < HT::NKH; ++kk)
-          if (hoff[kk] != 0xffffu) tq[kk] = ld4(oS + (int)hoff[kk] + X);
-#pragma unroll
-        for (int kk = 0; kk < HT::NKH; ++kk)
-          if (hoff[kk] != 0xffffu) st4(oS + (int)hoff[kk], tq[kk]);
+        constexpr int NCH = X / C1;                      // threads per step-1 row group
+        using HG = HaloTabG<H, HS, O2, PS>;
+        const int G = tid / NCH, li = tid % NCH;
+        const int cnt = kHaloTabG<H, HS, O2, PS>.cnt[G];
+#pragma unroll 2
+        for (int i = li; i < cnt; i += NCH) {
+          const int off = kHaloTabG<H, HS, O2, PS>.v[G][i];
+          st4(oS + off, ld4(oS + off + X));
+        }
+        (void)sizeof(HG);
       }
     }
   }
