@@ -245,9 +245,11 @@ __device__ __forceinline__ void mv1(const float2 (&M)[9], const float (&v)[3], f
 // (anticausal: E[n] = x[n] - x[n+1], E[n+1]).  xl = x[-1], x[-2]; xr = x[32], x[33].
 template <bool BETA>
 __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, float xl1, float xr0,
-                                            float xr1, const SweepIir& k, float2 (&yp)[32]) {
+                                            float xr1, const SweepIir& k, float2 (&yp)[32], float sx0 = 0.f,
+                                            float sx1 = 0.f, float sx2 = 0.f) {
+  // (sx0, sx1, sx2) = causal state (y[-1], y[-2], y[-3]) at the chunk start (0: zero state)
   float2 dprev = make_float2(xl0 - xl1, xr0 - xr1);
-  float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
+  float2 y1 = make_float2(sx0, 0.f), y2 = make_float2(sx1, 0.f), y3 = make_float2(sx2, 0.f);
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     float2 d;
@@ -269,41 +271,6 @@ __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, flo
     yp[i] = v;
   }
 }
-
-// Anticausal zero-state state at the left edge of a 32-sample chunk (true u: the
-// feedforward reads x[32], x[33]).  Packed halves: .x over samples [0,16), .y over
-// [16,32); the chunk state = lo + A^16 hi.
-template <bool BETA>
-__device__ __forceinline__ void chunk_anticausal_state(const float (&x)[32], float xn0, float xn1,
-                                                       const SweepIir& k, float (&va)[3]) {
-  float2 dprev = make_float2(x[16] - x[17], xn0 - xn1);
-  float2 y1 = make_float2(0.f, 0.f), y2 = y1, y3 = y1;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    float2 d;
-    d.x = x[15 - i] - x[16 - i];
-    d.y = x[31 - i] - (i == 0 ? xn0 : x[32 - i]);
-    float2 u = __fmul2_rn(k.c1, dprev);
-    u = __ffma2_rn(k.c0, d, u);
-    if (BETA) {
-      u.x = fmaf(k.beta.x, x[15 - i], u.x);
-      u.y = fmaf(k.beta.x, x[31 - i], u.y);
-    }
-    float2 v = __ffma2_rn(k.na3, y3, u);
-    v = __ffma2_rn(k.na2, y2, v);
-    v = __ffma2_rn(k.na1, y1, v);
-    y3 = y2;
-    y2 = y1;
-    y1 = v;
-    dprev = d;
-  }
-  const float hi[3] = {y1.y, y2.y, y3.y};
-  va[0] = y1.x;
-  va[1] = y2.x;
-  va[2] = y3.x;
-  mv1(k.M16, hi, va);
-}
-
 
 }  // namespace
 
@@ -543,6 +510,45 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           const float4 vl = ld4(rowF - 4);
           const float4 vr = ld4(rowF + 32);
           float2 yp[32];
+          if constexpr (TPR == 2) {
+            // Two chunks per tile row: chunk 0's causal recursion starts from the exact
+            // carry of the previous tile and chunk 1's anticausal one from the tile's
+            // right edge (zero state), so only chunk 1 .x and chunk 0 .y need an in-tile
+            // carry -- the partner chunk's end state (one exchange, no scan) -- and the
+            // fix-up runs on one lane per thread.
+            const bool c0 = (iq == 0);
+            chunk_sweep<BETA>(x, vl.w, vl.z, vr.x, vr.y, k, yp, c0 ? cin0 : 0.f, c0 ? cin1 : 0.f, c0 ? cin2 : 0.f);
+            const float e0 = c0 ? yp[31].x : yp[31].y, e1 = c0 ? yp[30].x : yp[30].y, e2 = c0 ? yp[29].x : yp[29].y;
+            // chunk 1 receives chunk 0's exact causal end state, chunk 0 chunk 1's
+            // zero-state anticausal state at its left edge
+            float h1 = __shfl_xor_sync(0xffffffffu, e0, 8);
+            float h2 = __shfl_xor_sync(0xffffffffu, e1, 8);
+            float h3 = __shfl_xor_sync(0xffffffffu, e2, 8);
+            const float2 msk = c0 ? make_float2(0.f, 1.f) : make_float2(1.f, 0.f);
+            const float na1 = k.na1.x, na2 = k.na2.x, na3 = k.na3.x;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float hh = na3 * h3;
+              hh = fmaf(na2, h2, hh);
+              hh = fmaf(na1, h1, hh);
+              h3 = h2;
+              h2 = h1;
+              h1 = hh;
+              yp[i] = __ffma2_rn(make_float2(hh, hh), msk, yp[i]);
+            }
+            // causal carry of the next tile: chunk 1's corrected end state; agg[t]:
+            // chunk 0's corrected anticausal state at the tile's left edge
+            const int src1 = lane | 8;
+            cin0 = __shfl_sync(0xffffffffu, yp[31].x, src1);
+            cin1 = __shfl_sync(0xffffffffu, yp[30].x, src1);
+            cin2 = __shfl_sync(0xffffffffu, yp[29].x, src1);
+            if (c0) {
+              const int o = oRing + (slot_t * H + ir) * 3;
+              sm[o] = yp[31].y;
+              sm[o + 1] = yp[30].y;
+              sm[o + 2] = yp[29].y;
+            }
+          } else {
           chunk_sweep<BETA>(x, vl.w, vl.z, vr.x, vr.y, k, yp);
           // carries: inclusive scan over the row's chunks, causal up (seeded with the
           // exact carry of the previous tile), anticausal down with zero state at the
@@ -624,6 +630,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
               yp[i] = __fadd2_rn(yp[i], h);
             }
           }
+          }   // TPR > 2
           // P(t) = y+ + y-_0 -> tensor memory slot
           // (the slot's previous content, P(t - D - 1), was loaded by the last back step)
           float P[32];
