@@ -162,6 +162,288 @@ __global__ void __launch_bounds__(FNT) k_fwd_b(const float* __restrict__ RA, flo
       if (s0 + vl < W) out[(long long)t * W + s0 + vl] = res[t * P + vl];
 }
 
+
+// ===========================================================================
+// Register-item forward passes (r02), levels split into two radix steps
+// R1 + R2 = log2(rows) <= 6, the back projection's item engine with the shift
+// direction of Eq.17.  For 2^R consecutive blocks of 2^l rows and a channel c
+// (the level-split identity of DESIGN.md §6, positive direction):
+//   out[c*2^R + r'][u] = sum_{b' < 2^R} in[b'*2^l + c][u + c*b' + d^(R)_{r'}(b')]
+// so step 1 (l = 0) runs R1 levels on row groups of 2^R1, step 2 (l = R1) runs R2
+// levels on the rows b'*2^R1 + c, pre-shifted by c*b' (addressing).  Items: 2^R
+// rows x 4 columns in registers, windows [v, v + 4 + O) read with LDS.128, levels
+// with compile-time shifts (FADD2 where the shift is even), the recursion's own
+// addition tree, so the results equal the level-by-level recursion bit for bit.
+//
+// One shared-memory tile of rows x (4 + W0) floats per CTA (tile of FX outputs plus
+// the right halo the shifts read, recomputed per tile).  Step 1 runs IN PLACE in
+// rounds of one item per thread: a round loads its windows, synchronises, then
+// stores, and rounds advance left to right inside every row group, so a round only
+// overwrites columns no later round reads.  Step 1 stores its output rows shifted
+// LEFT by their step-2 pre-shift mod 4 (physical = 4 + virtual - (c*b' & 3)), so
+// every step-2 window starts on a 16-byte boundary.  Step 2 stores float4 straight
+// to HBM.
+//   MODE 0 (pass A): rows y0 .. y0 + H of G_f (image rows, mirrored rows, image
+//           columns, mirrored columns) for u-tile columns -> R_A compact rows;
+//   MODE 1 (pass B): rows b of R_A[b][c][v + c*b] (pass-A channel c) -> linogram
+//           rows c*NB + t.
+// ===========================================================================
+constexpr int FNT2 = 256;
+
+template <int R, int C>
+struct ItP {
+  static constexpr int NR = 1 << R;
+  static constexpr int O = 4 * ((NR - 1 + 3) / 4);   // right halo >= 2^R - 1, whole quads
+  static constexpr int T = C + O;
+};
+
+__host__ __device__ constexpr int fpitch4(int w) { return (((w + 3) / 4) | 1) * 4; }
+
+template <int T2>
+__device__ __forceinline__ float colp(const float2 (&row)[T2], int t) {
+  return (t & 1) ? row[t >> 1].y : row[t >> 1].x;
+}
+
+// windows of rows b' = 0 .. 2^R - 1 at base + b'*rowstep, virtual start pre-shifted
+// by c*b'; the producer stored row b' shifted left by (c*b') & 3
+template <int R, int C>
+__device__ __forceinline__ void itemp_load(const float* base, int rowstep, int c,
+                                           float2 (&v)[ItP<R, C>::NR][ItP<R, C>::T / 2]) {
+  constexpr int NR = ItP<R, C>::NR, T = ItP<R, C>::T;
+  int cb = 0;
+#pragma unroll
+  for (int b = 0; b < NR; ++b) {
+    const float4* w = reinterpret_cast<const float4*>(base + b * rowstep + (cb & ~3));
+    cb += c;
+#pragma unroll
+    for (int q = 0; q < T / 4; ++q) {
+      const float4 f = w[q];
+      v[b][2 * q] = make_float2(f.x, f.y);
+      v[b][2 * q + 1] = make_float2(f.z, f.w);
+    }
+  }
+}
+
+// R levels, positive shifts: level h -> 2h
+//   w[blk + y'][t] = v[blk + lo][t] + v[blk + h + lo][t + ceil(y'/2)],  lo = floor(y'/2)
+// (the direction of Eq.17), computing after each level only the
+// columns [0, C + 2^R - 2^(lvl+1)) the outputs [0, C) still depend on.
+template <int R, int C>
+__device__ __forceinline__ void itemp_fht(float2 (&v)[ItP<R, C>::NR][ItP<R, C>::T / 2]) {
+  constexpr int NR = ItP<R, C>::NR, T2 = ItP<R, C>::T / 2;
+#pragma unroll
+  for (int lvl = 0; lvl < R; ++lvl) {
+    const int h = 1 << lvl;
+    const int ub2 = (C + NR - (2 << lvl)) / 2;
+    float2 w[NR][T2];
+#pragma unroll
+    for (int y = 0; y < NR; ++y) {
+      const int blk = y & ~(2 * h - 1);
+      const int yp = y - blk;
+      const int lo = yp >> 1;
+      const int sh = (yp + 1) >> 1;
+#pragma unroll
+      for (int tp = 0; tp < ub2; ++tp) {
+        const float2 a = v[blk + lo][tp];
+        if ((sh & 1) == 0) {
+          w[y][tp] = __fadd2_rn(a, v[blk + h + lo][tp + sh / 2]);
+        } else {
+          w[y][tp].x = a.x + colp(v[blk + h + lo], 2 * tp + sh);
+          w[y][tp].y = a.y + colp(v[blk + h + lo], 2 * tp + 1 + sh);
+        }
+      }
+    }
+#pragma unroll
+    for (int y = 0; y < NR; ++y)
+#pragma unroll
+      for (int tp = 0; tp < ub2; ++tp) v[y][tp] = w[y][tp];
+  }
+}
+
+template <int R1, int R2, int FX>
+struct FwdGeo {
+  static constexpr int ROWS = 1 << (R1 + R2);
+  static constexpr int N1 = 1 << R1, N2 = 1 << R2;
+  static constexpr int C = 4;
+  static constexpr int O1 = ItP<R1, C>::O, O2 = ItP<R2, C>::O;
+  // step-1 output columns step 2 reads: FX + max pre-shift + the step-2 window halo
+  static constexpr int W1 = (FX + (N1 - 1) * (N2 - 1) + O2 + 3) / 4 * 4;
+  static constexpr int W0 = W1 + O1;                 // input columns step 1 reads
+  static constexpr int P = fpitch4(4 + W0);          // 4 columns of room for the left shifts
+  static constexpr size_t smem = (size_t)ROWS * P * sizeof(float);
+};
+
+template <int R1, int R2, int FX, int MODE>
+__global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src, float* __restrict__ dst, int N,
+                                                   int H, int NB) {
+  using Gm = FwdGeo<R1, R2, FX>;
+  constexpr int ROWS = Gm::ROWS, N1 = Gm::N1, N2 = Gm::N2, C = Gm::C, P = Gm::P, W0 = Gm::W0, W1 = Gm::W1;
+  constexpr int NQ = W0 / 4;
+  extern __shared__ float4 fsm4[];
+  float* A = reinterpret_cast<float*>(fsm4);
+  const int tid = threadIdx.x;
+  const int sf = blockIdx.z;
+  const int WRF = N + H;
+  // ---- fill: virtual column v of row r at A[r*P + 4 + v] ----
+  if (MODE == 0) {
+    const int f = sf & 3, b = blockIdx.y;
+    const float* im = src + (long long)(sf >> 2) * N * N;
+    const int x0 = blockIdx.x * FX - H;               // x = u - N of virtual column 0
+    const int y0 = b * ROWS;
+    if (f < 2) {
+      // G_0[y][x] = img[y][x], G_1[y][x] = img[y][N-1-x]: lanes over quads of a row
+      for (int e = tid; e < ROWS * NQ; e += FNT2) {
+        const int j = e / NQ, q = e - j * NQ;
+        const int x = x0 + 4 * q;
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (x >= 0 && x < N) {
+          const float* row = im + (long long)(y0 + j) * N;
+          if (f == 0) {
+            val = __ldg(reinterpret_cast<const float4*>(row + x));
+          } else {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(row + N - 4 - x));
+            val = make_float4(t.w, t.z, t.y, t.x);
+          }
+        }
+        *reinterpret_cast<float4*>(A + j * P + 4 + 4 * q) = val;
+      }
+    } else {
+      // G_2[y][x] = img[x][y], G_3[y][x] = img[N-1-x][y]: lanes over rows j (the
+      // contiguous image axis), 4 columns per thread, one STS.128 (odd quad pitch:
+      // 8 consecutive rows hit 8 distinct bank groups)
+      for (int e = tid; e < ROWS * NQ; e += FNT2) {
+        const int q = e / ROWS, j = e - q * ROWS;
+        const int x = x0 + 4 * q;
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (x >= 0 && x < N) {
+          const float* colp0 = im + y0 + j;
+          if (f == 2) {
+            val.x = __ldg(colp0 + (long long)(x)*N);
+            val.y = __ldg(colp0 + (long long)(x + 1) * N);
+            val.z = __ldg(colp0 + (long long)(x + 2) * N);
+            val.w = __ldg(colp0 + (long long)(x + 3) * N);
+          } else {
+            val.x = __ldg(colp0 + (long long)(N - 1 - x) * N);
+            val.y = __ldg(colp0 + (long long)(N - 2 - x) * N);
+            val.z = __ldg(colp0 + (long long)(N - 3 - x) * N);
+            val.w = __ldg(colp0 + (long long)(N - 4 - x) * N);
+          }
+        }
+        *reinterpret_cast<float4*>(A + j * P + 4 + 4 * q) = val;
+      }
+    }
+  } else {
+    // rows b of G_c[b][v] = R_A[b][c][v + c*b] at compact column v + c*b - (N - H)
+    const int c = blockIdx.y, s0 = blockIdx.x * FX;
+    const float* in = src + (long long)sf * NB * H * WRF;
+    for (int e = tid; e < ROWS * NQ; e += FNT2) {
+      const int b = e / NQ, q = e - b * NQ;
+      const float* row = in + ((long long)b * H + c) * WRF;
+      const int j = s0 + 4 * q + c * b - (N - H);
+      float4 val;
+      val.x = (j >= 0 && j < WRF) ? __ldg(row + j) : 0.f;
+      val.y = (j + 1 >= 0 && j + 1 < WRF) ? __ldg(row + j + 1) : 0.f;
+      val.z = (j + 2 >= 0 && j + 2 < WRF) ? __ldg(row + j + 2) : 0.f;
+      val.w = (j + 3 >= 0 && j + 3 < WRF) ? __ldg(row + j + 3) : 0.f;
+      *reinterpret_cast<float4*>(A + b * P + 4 + 4 * q) = val;
+    }
+  }
+  __syncthreads();
+  // ---- step 1: R1 levels on row groups g (rows g*N1 ..), in place, in rounds ----
+  {
+    constexpr int NC1 = W1 / C, G1 = ROWS / N1, NI1 = NC1 * G1;
+    for (int base = 0; base < NI1; base += FNT2) {
+      const int it = base + tid;
+      const bool act = it < NI1;
+      const int g = act ? it / NC1 : 0, k = act ? it - g * NC1 : 0;
+      float2 v[N1][ItP<R1, C>::T / 2];
+      if (act) {
+        itemp_load<R1, C>(A + (g * N1) * P + 4 + C * k, P, 0, v);
+        itemp_fht<R1, C>(v);
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll
+        for (int r = 0; r < N1; ++r) {
+          const int sh = (r * g) & 3;                  // step-2 pre-shift of this row, mod 4
+          float* o = A + (g * N1 + r) * P + 4 + C * k - sh;
+          if (sh == 0) {
+            *reinterpret_cast<float4*>(o) = make_float4(colp(v[r], 0), colp(v[r], 1), colp(v[r], 2), colp(v[r], 3));
+          } else if (sh == 2) {
+            *reinterpret_cast<float2*>(o) = make_float2(colp(v[r], 0), colp(v[r], 1));
+            *reinterpret_cast<float2*>(o + 2) = make_float2(colp(v[r], 2), colp(v[r], 3));
+          } else {
+#pragma unroll
+            for (int tt = 0; tt < C; ++tt) o[tt] = colp(v[r], tt);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---- step 2: R2 levels on rows b'*N1 + c, pre-shift c*b' -> HBM ----
+  {
+    constexpr int NC2 = FX / C, NI2 = N1 * NC2;
+    for (int it = tid; it < NI2; it += FNT2) {
+      const int c = it / NC2, k = it - c * NC2;
+      float2 v[N2][ItP<R2, C>::T / 2];
+      itemp_load<R2, C>(A + c * P + 4 + C * k, N1 * P, c, v);
+      itemp_fht<R2, C>(v);
+      if (MODE == 0) {
+        const int b = blockIdx.y, j = blockIdx.x * FX + C * k;
+        if (j < WRF) {
+          float* out = dst + ((long long)sf * NB + b) * H * WRF + j;
+#pragma unroll
+          for (int r = 0; r < N2; ++r)
+            *reinterpret_cast<float4*>(out + (long long)(c * N2 + r) * WRF) =
+                make_float4(colp(v[r], 0), colp(v[r], 1), colp(v[r], 2), colp(v[r], 3));
+        }
+      } else {
+        const int ca = blockIdx.y, s = blockIdx.x * FX + C * k, W = 2 * N;
+        if (s < W) {
+          float* out = dst + ((long long)sf * N + (long long)ca * NB) * W + s;
+#pragma unroll
+          for (int r = 0; r < N2; ++r)
+            *reinterpret_cast<float4*>(out + (long long)(c * N2 + r) * W) =
+                make_float4(colp(v[r], 0), colp(v[r], 1), colp(v[r], 2), colp(v[r], 3));
+        }
+      }
+    }
+  }
+}
+
+// tile widths (output columns per CTA), ~64-72 KB of shared memory: 3 CTAs/SM
+template <int R1, int R2>
+struct FwdFX {
+  static constexpr int value = (R1 + R2 == 6) ? 192 : (R1 + R2 == 5) ? 448 : 960;
+};
+
+template <int R1, int R2, int MODE>
+cudaError_t launch_fwd_item(const float* src, float* dst, int slices, const Geometry& g, cudaStream_t st) {
+  constexpr int FX = FwdFX<R1, R2>::value;
+  using Gm = FwdGeo<R1, R2, FX>;
+  auto kern = k_fwd_item<R1, R2, FX, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::smem);
+  if (e != cudaSuccess) return e;
+  const int cols = MODE == 0 ? g.N + g.H : 2 * g.N;
+  const dim3 grid((cols + FX - 1) / FX, MODE == 0 ? g.NB : g.H, 4 * slices);
+  kern<<<grid, FNT2, Gm::smem, st>>>(src, dst, g.N, g.H, g.NB);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_fwd_item_rows(int rows, const float* src, float* dst, int slices, const Geometry& g,
+                                 cudaStream_t st) {
+  switch (rows) {
+    case 16: return launch_fwd_item<2, 2, MODE>(src, dst, slices, g, st);
+    case 32: return launch_fwd_item<3, 2, MODE>(src, dst, slices, g, st);
+    case 64: return launch_fwd_item<3, 3, MODE>(src, dst, slices, g, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+bool fwd_item_rows(int rows) { return rows == 16 || rows == 32 || rows == 64; }
+
 }  // namespace
 
 size_t fwd_workspace_floats(const Geometry& g) { return (size_t)4 * g.NB * g.H * (g.N + g.H); }
@@ -182,6 +464,10 @@ static int fwd_tile(int rows, int dflt, const char* env) {
 cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry& g, cudaStream_t st,
                          int* launches) {
   const int N = g.N, H = g.H, NB = g.NB;
+  if (fwd_item_rows(H)) {
+    if (launches) ++*launches;
+    return launch_fwd_item_rows<0>(H, img, RA, slices, g, st);
+  }
   const int FXA = fwd_tile(H, 64, "FBP_FXA");
   const size_t smem = (size_t)2 * H * (FXA + H + 1) * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -195,6 +481,10 @@ cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry
 cudaError_t launch_fwd_b(const float* RA, float* lin, int slices, const Geometry& g, cudaStream_t st,
                          int* launches) {
   const int N = g.N, H = g.H, NB = g.NB;
+  if (fwd_item_rows(NB)) {
+    if (launches) ++*launches;
+    return launch_fwd_item_rows<1>(NB, RA, lin, slices, g, st);
+  }
   const int FXB = fwd_tile(NB, NB <= 32 ? 256 : 128, "FBP_FXB");
   const size_t smem = (size_t)2 * NB * (FXB + NB + 1) * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

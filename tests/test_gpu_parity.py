@@ -401,6 +401,37 @@ def test_forward_integer_bit_exact(fbp, N):
         assert np.array_equal(out[i].astype(np.float64), ref), (N, i)
 
 
+@pytest.mark.parametrize("N,B", [(1024, 2), (2048, 1)])
+def test_forward_integer_bit_exact_item_path(fbp, N, B):
+    """The register-item forward passes (k_fwd_item: rows 16/32/64, i.e. N = 512..8192)
+    over whole images at the bench size: every sample equals the oracle's fht_forward
+    (Eq.17 recursion) exactly on integer images, several tiles, the ragged last
+    u-tile of pass A (N + H not a multiple of the tile) and the slice index."""
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=B)
+    img = P.integer_image(N, B, seed=3 * N + 1, lo=-7, hi=7)
+    out = plan.forward(img.cuda()).cpu().numpy()
+    for i in range(B):
+        ref = O.fht_forward(img[i].numpy().astype(np.float64))
+        assert np.array_equal(out[i].astype(np.float64), ref), (N, i)
+
+
+def test_forward_4096_sampled(fbp):
+    """N = 4096 (pass B with 64 rows per channel, radix 8 + 8): sampled outputs of
+    all four families exact vs the direct definition on an integer image."""
+    N = 4096
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=1)
+    img = P.integer_image(N, 1, seed=4096, lo=-7, hi=7)
+    S = plan.forward(img.cuda()).cpu()[0]
+    im = img[0].numpy().astype(np.float64)
+    rng = np.random.default_rng(41)
+    for _ in range(16):
+        f, t, s_ = int(rng.integers(4)), int(rng.integers(N)), int(rng.integers(2 * N))
+        assert float(S[f, t, s_]) == O.forward_sample(im, f, t, s_), (f, t, s_)
+    assert np.all(S.double().sum(dim=2).numpy() == im.sum())
+
+
 @pytest.mark.parametrize("N", [64, 1024])
 def test_forward_float_within_tolerance(fbp, N):
     """Random float images: fp32 sums vs fp64 oracle within the 1e-4 gate (samples at
