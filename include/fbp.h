@@ -104,8 +104,10 @@ FBP_API fbp_status fbp_fht_backproject(const fbp_plan* plan, const float* lin, f
  *   image: device [batch][N][N];  lin: device [batch][4][N][2N] (overwritten).
  *   Additions only (bit-exact on integer-valued input); the exact adjoint of
  *   fbp_fht_backproject's per-family sums.  Uses the plan's workspace, so calls on
- *   one plan must not run concurrently.  Errors: FBP_ERR_PARAM (NULL / misaligned
- *   pointer, batch outside [0, max_batch]), FBP_ERR_CUDA.
+ *   one plan must not run concurrently; lin doubles as scratch (the transposed
+ *   image), so image and lin must not overlap.  Errors: FBP_ERR_PARAM (NULL /
+ *   misaligned pointer, batch outside [0, max_batch], overlapping buffers),
+ *   FBP_ERR_CUDA.
  */
 FBP_API fbp_status fbp_fht_forward(const fbp_plan* plan, const float* image, float* lin, int batch,
                                    void* cuda_stream);

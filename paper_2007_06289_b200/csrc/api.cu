@@ -547,12 +547,15 @@ fbp_status fbp_fht_forward(const fbp_plan* p, const float* image, float* lin, in
   int launches = 0;
   const long long lin_elems = 4LL * p->g.N * p->g.W;
   const long long img_elems = (long long)p->g.N * p->g.N;
+  // lin also stages the transposed image of pass A: the buffers must not overlap
+  if (image < lin + batch * lin_elems && lin < image + batch * img_elems)
+    return fail(FBP_ERR_PARAM, "fbp_fht_forward: image and lin overlap");
   const size_t per = fwd_workspace_floats(p->g) * sizeof(float);
   const int grp = (int)std::max<size_t>(1, std::min<size_t>(p->R_bytes / per, 16383));
   const cudaStream_t st = (cudaStream_t)stream;
   for (int s0 = 0; s0 < batch; s0 += grp) {
     const int ns = std::min(grp, batch - s0);
-    cudaError_t e = timed(p, 3, st, [&] { return launch_fwd_a(image + s0 * img_elems, p->R, ns, p->g, st, &launches); });
+    cudaError_t e = timed(p, 3, st, [&] { return launch_fwd_a(image + s0 * img_elems, p->R, lin + s0 * lin_elems, ns, p->g, st, &launches); });
     if (e == cudaSuccess)
       e = timed(p, 4, st, [&] { return launch_fwd_b(p->R, lin + s0 * lin_elems, ns, p->g, st, &launches); });
     if (e != cudaSuccess) {

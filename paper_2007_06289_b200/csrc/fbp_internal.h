@@ -119,7 +119,7 @@ size_t fwd_workspace_floats(const Geometry& g);
 // -> lin [slices][4][N][2N].  slices <= 16383.
 cudaError_t launch_resample(const float* sino, float* lin, int slices, int n_angles, int n_bins, double dr,
                             const Geometry& g, cudaStream_t st, int* launches);
-cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry& g, cudaStream_t st,
+cudaError_t launch_fwd_a(const float* img, float* RA, float* scratch, int slices, const Geometry& g, cudaStream_t st,
                          int* launches);
 cudaError_t launch_fwd_b(const float* RA, float* lin, int slices, const Geometry& g, cudaStream_t st,
                          int* launches);

@@ -183,12 +183,43 @@ __global__ void __launch_bounds__(FNT) k_fwd_b(const float* __restrict__ RA, flo
 // LEFT by their step-2 pre-shift mod 4 (physical = 4 + virtual - (c*b' & 3)), so
 // every step-2 window starts on a 16-byte boundary.  Step 2 stores float4 straight
 // to HBM.
-//   MODE 0 (pass A): rows y0 .. y0 + H of G_f (image rows, mirrored rows, image
-//           columns, mirrored columns) for u-tile columns -> R_A compact rows;
+//   MODE 0 (pass A): rows y0 .. y0 + H of G_f for u-tile columns -> R_A rows.
+//           G_0/G_2 are rows of the image / of its transpose (k_transpose, staged
+//           in the linogram output, which pass B overwrites later); G_1/G_3 the
+//           same rows mirrored: their aligned quads are copied as they are (so
+//           each quad lands reversed) and step 1 undoes the reversal in registers.
+//           Every fill is a 16-byte cp.async.
 //   MODE 1 (pass B): rows b of R_A[b][c][v + c*b] (pass-A channel c) -> linogram
 //           rows c*NB + t.
+// R_A layout (item path): row (b, t') of width WRF2 = N + H + 4 holds logical
+// compact column j (u = N - H + j, j < N + H) at j + ((-t'*b) & 3), zeros in the
+// pad, so that pass B's pre-shifted rows start on 16-byte boundaries (every pass-B
+// fill quad is one aligned 16-byte copy); pass A stores with the row's alignment
+// (STG.128, 2 x STG.64 or 4 x STG.32).
 // ===========================================================================
 constexpr int FNT2 = 256;
+
+// asynchronous global -> shared copy (LDGSTS, no register round trip); 0 source
+// bytes zero-fill the destination (the source address is then not read)
+__device__ __forceinline__ void cpa16(float* dst, const float* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+// explicit global stores (the widths chosen from the row's alignment must not be
+// merged by the compiler)
+__device__ __forceinline__ void stg1(float* g, float a) {
+  asm volatile("st.global.f32 [%0], %1;\n" ::"l"(g), "f"(a) : "memory");
+}
+__device__ __forceinline__ void stg2(float* g, float a, float b) {
+  asm volatile("st.global.v2.f32 [%0], {%1, %2};\n" ::"l"(g), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void stg4(float* g, float a, float b, float c, float d) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(g), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 
 template <int R, int C>
 struct ItP {
@@ -206,7 +237,9 @@ __device__ __forceinline__ float colp(const float2 (&row)[T2], int t) {
 
 // windows of rows b' = 0 .. 2^R - 1 at base + b'*rowstep, virtual start pre-shifted
 // by c*b'; the producer stored row b' shifted left by (c*b') & 3
-template <int R, int C>
+// REV: every quad was stored reversed (mirrored families, see the fill); the
+// reversal is undone by register naming.
+template <int R, int C, bool REV = false>
 __device__ __forceinline__ void itemp_load(const float* base, int rowstep, int c,
                                            float2 (&v)[ItP<R, C>::NR][ItP<R, C>::T / 2]) {
   constexpr int NR = ItP<R, C>::NR, T = ItP<R, C>::T;
@@ -218,8 +251,8 @@ __device__ __forceinline__ void itemp_load(const float* base, int rowstep, int c
 #pragma unroll
     for (int q = 0; q < T / 4; ++q) {
       const float4 f = w[q];
-      v[b][2 * q] = make_float2(f.x, f.y);
-      v[b][2 * q + 1] = make_float2(f.z, f.w);
+      v[b][2 * q] = REV ? make_float2(f.w, f.z) : make_float2(f.x, f.y);
+      v[b][2 * q + 1] = REV ? make_float2(f.y, f.x) : make_float2(f.z, f.w);
     }
   }
 }
@@ -264,8 +297,11 @@ template <int R1, int R2, int FX>
 struct FwdGeo {
   static constexpr int ROWS = 1 << (R1 + R2);
   static constexpr int N1 = 1 << R1, N2 = 1 << R2;
-  static constexpr int C = 4;
-  static constexpr int O1 = ItP<R1, C>::O, O2 = ItP<R2, C>::O;
+  static constexpr int C = 4;                        // step-1 item columns
+  // step-2 item columns (8 for radix 4 measured slower: 1.02 vs 0.77 ms, lanes 32 B
+  // apart conflict in LDS.128 and half-fill each store's sectors)
+  static constexpr int C2 = 4;
+  static constexpr int O1 = ItP<R1, C>::O, O2 = ItP<R2, C2>::O;
   // step-1 output columns step 2 reads: FX + max pre-shift + the step-2 window halo
   static constexpr int W1 = (FX + (N1 - 1) * (N2 - 1) + O2 + 3) / 4 * 4;
   static constexpr int W0 = W1 + O1;                 // input columns step 1 reads
@@ -274,80 +310,45 @@ struct FwdGeo {
 };
 
 template <int R1, int R2, int FX, int MODE>
-__global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src, float* __restrict__ dst, int N,
-                                                   int H, int NB) {
+__global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src, const float* __restrict__ srcT,
+                                                   float* __restrict__ dst, int N, int H, int NB) {
   using Gm = FwdGeo<R1, R2, FX>;
-  constexpr int ROWS = Gm::ROWS, N1 = Gm::N1, N2 = Gm::N2, C = Gm::C, P = Gm::P, W0 = Gm::W0, W1 = Gm::W1;
+  constexpr int ROWS = Gm::ROWS, N1 = Gm::N1, N2 = Gm::N2, C = Gm::C, C2 = Gm::C2, P = Gm::P, W0 = Gm::W0,
+                W1 = Gm::W1;
   constexpr int NQ = W0 / 4;
   extern __shared__ float4 fsm4[];
   float* A = reinterpret_cast<float*>(fsm4);
   const int tid = threadIdx.x;
   const int sf = blockIdx.z;
-  const int WRF = N + H;
-  // ---- fill: virtual column v of row r at A[r*P + 4 + v] ----
+  const int WRF = N + H, WRF2 = N + H + 4;
+  // ---- fill: virtual column v of row r at A[r*P + 4 + v], cp.async (zero outside) ----
   if (MODE == 0) {
     const int f = sf & 3, b = blockIdx.y;
-    const float* im = src + (long long)(sf >> 2) * N * N;
+    const float* im = (f < 2 ? src : srcT) + (long long)(sf >> 2) * N * N;
     const int x0 = blockIdx.x * FX - H;               // x = u - N of virtual column 0
     const int y0 = b * ROWS;
-    if (f < 2) {
-      // G_0[y][x] = img[y][x], G_1[y][x] = img[y][N-1-x]: lanes over quads of a row
-      for (int e = tid; e < ROWS * NQ; e += FNT2) {
-        const int j = e / NQ, q = e - j * NQ;
-        const int x = x0 + 4 * q;
-        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (x >= 0 && x < N) {
-          const float* row = im + (long long)(y0 + j) * N;
-          if (f == 0) {
-            val = __ldg(reinterpret_cast<const float4*>(row + x));
-          } else {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(row + N - 4 - x));
-            val = make_float4(t.w, t.z, t.y, t.x);
-          }
-        }
-        *reinterpret_cast<float4*>(A + j * P + 4 + 4 * q) = val;
-      }
-    } else {
-      // G_2[y][x] = img[x][y], G_3[y][x] = img[N-1-x][y]: lanes over rows j (the
-      // contiguous image axis), 4 columns per thread, one STS.128 (odd quad pitch:
-      // 8 consecutive rows hit 8 distinct bank groups)
-      for (int e = tid; e < ROWS * NQ; e += FNT2) {
-        const int q = e / ROWS, j = e - q * ROWS;
-        const int x = x0 + 4 * q;
-        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (x >= 0 && x < N) {
-          const float* colp0 = im + y0 + j;
-          if (f == 2) {
-            val.x = __ldg(colp0 + (long long)(x)*N);
-            val.y = __ldg(colp0 + (long long)(x + 1) * N);
-            val.z = __ldg(colp0 + (long long)(x + 2) * N);
-            val.w = __ldg(colp0 + (long long)(x + 3) * N);
-          } else {
-            val.x = __ldg(colp0 + (long long)(N - 1 - x) * N);
-            val.y = __ldg(colp0 + (long long)(N - 2 - x) * N);
-            val.z = __ldg(colp0 + (long long)(N - 3 - x) * N);
-            val.w = __ldg(colp0 + (long long)(N - 4 - x) * N);
-          }
-        }
-        *reinterpret_cast<float4*>(A + j * P + 4 + 4 * q) = val;
-      }
+    for (int e = tid; e < ROWS * NQ; e += FNT2) {
+      const int j = e / NQ, q = e - j * NQ;
+      const int x = x0 + 4 * q;
+      const bool ok = x >= 0 && x < N;
+      // G[y][x .. x+3] = row[x .. x+3], or for the mirrored views row[N-4-x .. N-1-x]
+      // (reversed)
+      const int gx = (f & 1) ? N - 4 - x : x;
+      cpa16(A + j * P + 4 + 4 * q, im + (long long)(y0 + j) * N + (ok ? gx : 0), ok);
     }
   } else {
-    // rows b of G_c[b][v] = R_A[b][c][v + c*b] at compact column v + c*b - (N - H)
+    // rows b of G_c[b][v] = R_A[b][c][v + c*b]: logical column v + c*b - (N - H) at
+    // physical v - (N - H) + 4*ceil(c*b/4), a multiple of 4
     const int c = blockIdx.y, s0 = blockIdx.x * FX;
-    const float* in = src + (long long)sf * NB * H * WRF;
+    const float* in = src + (long long)sf * NB * H * WRF2;
     for (int e = tid; e < ROWS * NQ; e += FNT2) {
       const int b = e / NQ, q = e - b * NQ;
-      const float* row = in + ((long long)b * H + c) * WRF;
-      const int j = s0 + 4 * q + c * b - (N - H);
-      float4 val;
-      val.x = (j >= 0 && j < WRF) ? __ldg(row + j) : 0.f;
-      val.y = (j + 1 >= 0 && j + 1 < WRF) ? __ldg(row + j + 1) : 0.f;
-      val.z = (j + 2 >= 0 && j + 2 < WRF) ? __ldg(row + j + 2) : 0.f;
-      val.w = (j + 3 >= 0 && j + 3 < WRF) ? __ldg(row + j + 3) : 0.f;
-      *reinterpret_cast<float4*>(A + b * P + 4 + 4 * q) = val;
+      const int pp = s0 + 4 * q - (N - H) + 4 * ((c * b + 3) >> 2);
+      const bool ok = pp >= 0 && pp + 4 <= WRF2;
+      cpa16(A + b * P + 4 + 4 * q, in + ((long long)b * H + c) * WRF2 + (ok ? pp : 0), ok);
     }
   }
+  cpa_wait_all();
   __syncthreads();
   // ---- step 1: R1 levels on row groups g (rows g*N1 ..), in place, in rounds ----
   {
@@ -358,7 +359,10 @@ __global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src
       const int g = act ? it / NC1 : 0, k = act ? it - g * NC1 : 0;
       float2 v[N1][ItP<R1, C>::T / 2];
       if (act) {
-        itemp_load<R1, C>(A + (g * N1) * P + 4 + C * k, P, 0, v);
+        if (MODE == 0 && (sf & 1))
+          itemp_load<R1, C, true>(A + (g * N1) * P + 4 + C * k, P, 0, v);
+        else
+          itemp_load<R1, C>(A + (g * N1) * P + 4 + C * k, P, 0, v);
         itemp_fht<R1, C>(v);
       }
       __syncthreads();
@@ -383,29 +387,58 @@ __global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src
   }
   // ---- step 2: R2 levels on rows b'*N1 + c, pre-shift c*b' -> HBM ----
   {
-    constexpr int NC2 = FX / C, NI2 = N1 * NC2;
+    constexpr int NC2 = FX / C2, NI2 = N1 * NC2;
     for (int it = tid; it < NI2; it += FNT2) {
       const int c = it / NC2, k = it - c * NC2;
-      float2 v[N2][ItP<R2, C>::T / 2];
-      itemp_load<R2, C>(A + c * P + 4 + C * k, N1 * P, c, v);
-      itemp_fht<R2, C>(v);
+      float2 v[N2][ItP<R2, C2>::T / 2];
+      itemp_load<R2, C2>(A + c * P + 4 + C2 * k, N1 * P, c, v);
+      itemp_fht<R2, C2>(v);
       if (MODE == 0) {
-        const int b = blockIdx.y, j = blockIdx.x * FX + C * k;
-        if (j < WRF) {
-          float* out = dst + ((long long)sf * NB + b) * H * WRF + j;
+        const int b = blockIdx.y;
+        float* out = dst + ((long long)sf * NB + b) * H * WRF2;
 #pragma unroll
-          for (int r = 0; r < N2; ++r)
-            *reinterpret_cast<float4*>(out + (long long)(c * N2 + r) * WRF) =
-                make_float4(colp(v[r], 0), colp(v[r], 1), colp(v[r], 2), colp(v[r], 3));
+        for (int hq = 0; hq < C2 / 4; ++hq) {
+          const int j = blockIdx.x * FX + C2 * k + 4 * hq;
+          if (j < WRF) {
+#pragma unroll
+            for (int r = 0; r < N2; ++r) {
+              const int t = c * N2 + r;
+              const int sh = (-(t * b)) & 3;
+              float* row = out + (long long)t * WRF2;
+              float* o = row + j + sh;
+              const float a0 = colp(v[r], 4 * hq), a1 = colp(v[r], 4 * hq + 1), a2 = colp(v[r], 4 * hq + 2),
+                          a3 = colp(v[r], 4 * hq + 3);
+              if (sh == 0) {
+                stg4(o, a0, a1, a2, a3);
+              } else if (sh == 2) {
+                stg2(o, a0, a1);
+                stg2(o + 2, a2, a3);
+              } else {
+                stg1(o, a0);
+                stg1(o + 1, a1);
+                stg1(o + 2, a2);
+                stg1(o + 3, a3);
+              }
+              // zero pad: [0, sh) before the row, [WRF + sh, WRF2) after it
+              if (j == 0)
+                for (int i = 0; i < sh; ++i) stg1(row + i, 0.f);
+              if (j + 4 == WRF)
+                for (int i = WRF + sh; i < WRF2; ++i) stg1(row + i, 0.f);
+            }
+          }
         }
       } else {
-        const int ca = blockIdx.y, s = blockIdx.x * FX + C * k, W = 2 * N;
-        if (s < W) {
-          float* out = dst + ((long long)sf * N + (long long)ca * NB) * W + s;
+        const int ca = blockIdx.y, W = 2 * N;
+        float* out = dst + ((long long)sf * N + (long long)ca * NB) * W;
 #pragma unroll
-          for (int r = 0; r < N2; ++r)
-            *reinterpret_cast<float4*>(out + (long long)(c * N2 + r) * W) =
-                make_float4(colp(v[r], 0), colp(v[r], 1), colp(v[r], 2), colp(v[r], 3));
+        for (int hq = 0; hq < C2 / 4; ++hq) {
+          const int s = blockIdx.x * FX + C2 * k + 4 * hq;
+          if (s < W) {
+#pragma unroll
+            for (int r = 0; r < N2; ++r)
+              stg4(out + (long long)(c * N2 + r) * W + s, colp(v[r], 4 * hq), colp(v[r], 4 * hq + 1),
+                   colp(v[r], 4 * hq + 2), colp(v[r], 4 * hq + 3));
+          }
         }
       }
     }
@@ -419,7 +452,8 @@ struct FwdFX {
 };
 
 template <int R1, int R2, int MODE>
-cudaError_t launch_fwd_item(const float* src, float* dst, int slices, const Geometry& g, cudaStream_t st) {
+cudaError_t launch_fwd_item(const float* src, const float* srcT, float* dst, int slices, const Geometry& g,
+                            cudaStream_t st) {
   constexpr int FX = FwdFX<R1, R2>::value;
   using Gm = FwdGeo<R1, R2, FX>;
   auto kern = k_fwd_item<R1, R2, FX, MODE>;
@@ -427,26 +461,43 @@ cudaError_t launch_fwd_item(const float* src, float* dst, int slices, const Geom
   if (e != cudaSuccess) return e;
   const int cols = MODE == 0 ? g.N + g.H : 2 * g.N;
   const dim3 grid((cols + FX - 1) / FX, MODE == 0 ? g.NB : g.H, 4 * slices);
-  kern<<<grid, FNT2, Gm::smem, st>>>(src, dst, g.N, g.H, g.NB);
+  kern<<<grid, FNT2, Gm::smem, st>>>(src, srcT, dst, g.N, g.H, g.NB);
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_fwd_item_rows(int rows, const float* src, float* dst, int slices, const Geometry& g,
-                                 cudaStream_t st) {
+cudaError_t launch_fwd_item_rows(int rows, const float* src, const float* srcT, float* dst, int slices,
+                                 const Geometry& g, cudaStream_t st) {
   switch (rows) {
-    case 16: return launch_fwd_item<2, 2, MODE>(src, dst, slices, g, st);
-    case 32: return launch_fwd_item<3, 2, MODE>(src, dst, slices, g, st);
-    case 64: return launch_fwd_item<3, 3, MODE>(src, dst, slices, g, st);
+    case 16: return launch_fwd_item<2, 2, MODE>(src, srcT, dst, slices, g, st);
+    case 32: return launch_fwd_item<3, 2, MODE>(src, srcT, dst, slices, g, st);
+    case 64: return launch_fwd_item<3, 3, MODE>(src, srcT, dst, slices, g, st);
     default: return cudaErrorNotSupported;
   }
 }
 
 bool fwd_item_rows(int rows) { return rows == 16 || rows == 32 || rows == 64; }
 
+// item path for both passes (N = 512 .. 4096); otherwise the shared-memory kernels
+bool fwd_item_path(const Geometry& g) { return fwd_item_rows(g.H) && fwd_item_rows(g.NB); }
+
+// image transpose [slices][N][N] (families 2 and 3 read image columns as rows):
+// 32 x 32 tiles through shared memory (odd pitch), coalesced on both sides
+__global__ void __launch_bounds__(256) k_transpose(const float* __restrict__ in, float* __restrict__ out, int N) {
+  __shared__ float t[32][33];
+  const long long off = (long long)blockIdx.z * N * N;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) t[ty + k][tx] = __ldg(in + off + (long long)(y0 + ty + k) * N + x0 + tx);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) out[off + (long long)(x0 + ty + k) * N + y0 + tx] = t[tx][ty + k];
+}
+
 }  // namespace
 
-size_t fwd_workspace_floats(const Geometry& g) { return (size_t)4 * g.NB * g.H * (g.N + g.H); }
+size_t fwd_workspace_floats(const Geometry& g) { return (size_t)4 * g.NB * g.H * (g.N + g.H + 4); }
 
 // output columns per tile (a multiple of 32): wide enough that the right halo
 // (H - 1, resp. NB - 1 columns) is a small overhead, narrow enough for >= 2 CTAs/SM
@@ -461,12 +512,15 @@ static int fwd_tile(int rows, int dflt, const char* env) {
   return x;
 }
 
-cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry& g, cudaStream_t st,
-                         int* launches) {
+cudaError_t launch_fwd_a(const float* img, float* RA, float* scratch, int slices, const Geometry& g,
+                         cudaStream_t st, int* launches) {
   const int N = g.N, H = g.H, NB = g.NB;
-  if (fwd_item_rows(H)) {
-    if (launches) ++*launches;
-    return launch_fwd_item_rows<0>(H, img, RA, slices, g, st);
+  if (fwd_item_path(g)) {
+    k_transpose<<<dim3(N / 32, N / 32, slices), 256, 0, st>>>(img, scratch, N);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 2;
+    return launch_fwd_item_rows<0>(H, img, scratch, RA, slices, g, st);
   }
   const int FXA = fwd_tile(H, 64, "FBP_FXA");
   const size_t smem = (size_t)2 * H * (FXA + H + 1) * sizeof(float);
@@ -481,9 +535,9 @@ cudaError_t launch_fwd_a(const float* img, float* RA, int slices, const Geometry
 cudaError_t launch_fwd_b(const float* RA, float* lin, int slices, const Geometry& g, cudaStream_t st,
                          int* launches) {
   const int N = g.N, H = g.H, NB = g.NB;
-  if (fwd_item_rows(NB)) {
+  if (fwd_item_path(g)) {
     if (launches) ++*launches;
-    return launch_fwd_item_rows<1>(NB, RA, lin, slices, g, st);
+    return launch_fwd_item_rows<1>(NB, RA, nullptr, lin, slices, g, st);
   }
   const int FXB = fwd_tile(NB, NB <= 32 ? 256 : 128, "FBP_FXB");
   const size_t smem = (size_t)2 * NB * (FXB + NB + 1) * sizeof(float);

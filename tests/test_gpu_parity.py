@@ -487,6 +487,10 @@ def test_forward_edge_cases(fbp):
         plan.forward(torch.zeros((1, N, 2 * N), device="cuda")[:, :, ::2])
     with pytest.raises(fbp.FbpError):
         plan.forward(torch.zeros((3, N, N), device="cuda"))       # batch > max_batch
+    # lin stages the transposed image: overlapping buffers are refused
+    buf = torch.zeros(8 * N * N + N * N, device="cuda")
+    with pytest.raises(fbp.FbpError):
+        plan.forward(buf[: N * N].view(1, N, N), out=buf[N * N // 2: N * N // 2 + 8 * N * N].view(1, 4, N, 2 * N))
     # a single unit pixel lights exactly one sample per (family, t) row
     img = torch.zeros((1, N, N), device="cuda")
     img[0, 5, 9] = 1.0

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Per-CUDA-source-line profile of one kernel from an ncu report (no GPU needed).
 
-  python tools/ncu_lines.py report.ncu-rep k_sweep_a [top] [--ranges a-b:name,...]
+  python tools/ncu_lines.py report.ncu-rep k_sweep_a [top] [--ranges a-b:name,...] [--skip=i]
 Prints instructions executed and warp-stall samples per source line (top lines),
 the stall-reason mix, and optional line-range totals (kernel regions).
 Needs a capture with --import-source on and a -lineinfo build.
@@ -14,14 +14,17 @@ import sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 30
 ranges = []
+extra = []
 for a in sys.argv[3:]:
+    if a.startswith("--skip="):
+        extra = ["--launch-skip", a.split("=", 1)[1], "--launch-count", "1"]
     if a.startswith("--ranges="):
         for part in a.split("=", 1)[1].split(","):
             lr, name = part.split(":")
             lo, hi = lr.split("-")
             ranges.append((int(lo), int(hi), name))
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}",
-                      "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
+                      "--print-source", "cuda,sass"] + extra, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 files = []
 cur = None
