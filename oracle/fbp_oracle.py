@@ -37,6 +37,7 @@ __all__ = [
     "dyadic_offsets_closed_form", "dyadic_offsets_column", "family_views", "forward_project",
     "backproject_direct", "backproject_pixel", "fht_backproject", "combine",
     "reconstruct", "iir_poles", "fht_forward",
+    "ramp_filter_rtheta", "backproject_rtheta", "fbp_rtheta",
 ]
 
 
@@ -473,6 +474,59 @@ def resample_sinogram(p: np.ndarray, N: int, dr: float = 1.0) -> np.ndarray:
                 r, th, L = linogram_line_rtheta(f, t, s, N)
                 S[f, t, s] = sinogram_sample(p, th, r, dr) / L
     return S
+
+
+# --------------------------------------------------------------------------
+# §2  Conventional (r, theta) FBP — the NEXT-4 comparison baseline
+# --------------------------------------------------------------------------
+
+def ramp_filter_rtheta(p: np.ndarray, dr: float = 1.0, L0: int | None = None) -> np.ndarray:
+    """Ramp-filter every projection row of a scanner sinogram p[k][j] (Eq.3, Eq.8).
+
+    PAPER.md:63-66 (Eq.3) with the band-limited kernel of Eq.7
+    sampled at bin spacing dr (R24): q(r_j) = dr * sum_m h_dr(m) p(r_{j-m}),
+    h_dr(m) = h(m) / dr^2.  L0 defaults to R (the kernel covers the whole row).
+    """
+    p = np.asarray(p, dtype=np.float64)
+    R = p.shape[-1]
+    taps = ramp_kernel(R if L0 is None else L0) / (dr * dr)
+    return dr * fir_filter(p, taps)
+
+
+def backproject_rtheta(q: np.ndarray, N: int, dr: float = 1.0) -> np.ndarray:
+    """Direct back projection in (r, theta), Theta(N^2 P) (Eq.5, R24).
+
+    PAPER.md:72-77 (Eq.5): f(x, y) = integral over theta of q_theta(x cos theta +
+    y sin theta); discretised on the P angles theta_k = k pi / P in [0, pi) with
+    weight pi / P: p(r, theta + pi) = p(-r, theta) folds Eq.5's [0, 2 pi) onto
+    [0, pi), and the inversion with the |omega| kernel of Eq.4 integrates one
+    half-turn (Eq.5's missing 1/2, reading R24); q linear in r (bins outside the detector read 0).
+    Pixel (y, x) sits at (x + 0.5, y + 0.5), r measured from the centre (N/2, N/2)
+    (the geometry of R23).  Returns img[y][x].
+    """
+    q = np.asarray(q, dtype=np.float64)
+    P, R = q.shape
+    c = np.arange(N) + 0.5 - N / 2.0
+    X, Y = np.meshgrid(c, c)            # X[y][x] = x + 0.5 - N/2, Y[y][x] = y + 0.5 - N/2
+    img = np.zeros((N, N))
+    for k in range(P):
+        th = k * math.pi / P
+        w = (X * math.cos(th) + Y * math.sin(th)) / dr + 0.5 * (R - 1)
+        j0 = np.floor(w).astype(np.int64)
+        a = w - j0
+        row = np.concatenate([[0.0], q[k], [0.0]])       # index j + 1; 0 outside [0, R)
+        i0 = np.clip(j0 + 1, 0, R + 1)
+        i1 = np.clip(j0 + 2, 0, R + 1)
+        img += (1.0 - a) * row[i0] + a * row[i1]
+    return img * (math.pi / P)
+
+
+def fbp_rtheta(p: np.ndarray, N: int, dr: float = 1.0) -> np.ndarray:
+    """Conventional FBP on a scanner sinogram: Eq.3 filtering, then Eq.5 direct
+    back projection ("the sequential application of two
+    operations"); the Theta(N^3) "Radon" back projection of Fig. 2b
+    (PAPER.md:238, 273), the NEXT-4 comparison baseline."""
+    return backproject_rtheta(ramp_filter_rtheta(p, dr), N, dr)
 
 
 def combine(B: np.ndarray, w: float) -> np.ndarray:

@@ -443,3 +443,96 @@ def test_resample_ellipses_close_to_analytic_linogram():
     sino = P.sinogram_of_ellipses(E, N, 4 * N, int(math.ceil(N * math.sqrt(2) / 0.5)) + 4, 0.5).numpy()
     S = O.resample_sinogram(sino, N, 0.5)
     assert math.sqrt(((S - ref) ** 2).mean()) / math.sqrt((ref ** 2).mean()) < 0.02
+
+
+# ------------------------------------------- NEXT-4: conventional (r, theta) FBP
+def test_backproject_rtheta_single_angle_smears():
+    """Eq.5 with one nonzero angle: the back projection of a row
+    that is linear in the bin index is constant along the line direction and equals
+    pi/P times the row at r = x.n (linear interpolation is exact on a linear row).
+    theta = 0 (normal +x): constant down columns; theta = pi/2 (normal +y): constant
+    along rows.  Pins the angle origin, the centre (N/2, N/2) and the pi/P weight."""
+    N, P, R = 16, 8, 40
+    c = np.arange(N) + 0.5 - N / 2.0
+    q = np.zeros((P, R))
+    q[0] = np.arange(R) * 2.0 + 1.0              # value 2j + 1 at bin j
+    img = O.backproject_rtheta(q, N)
+    expect_x = math.pi / P * (2.0 * (c + 0.5 * (R - 1)) + 1.0)
+    assert np.allclose(img, np.broadcast_to(expect_x[None, :], (N, N)), atol=1e-12)
+    q = np.zeros((P, R))
+    q[P // 2] = np.arange(R) * 2.0 + 1.0
+    img = O.backproject_rtheta(q, N, dr=0.5)     # bin j at r = (j - (R-1)/2) / 2
+    expect_y = math.pi / P * (2.0 * (2.0 * c + 0.5 * (R - 1)) + 1.0)
+    assert np.allclose(img, np.broadcast_to(expect_y[:, None], (N, N)), atol=1e-12)
+
+
+def test_backproject_rtheta_constant_and_outside():
+    """A constant sinogram back-projects to pi * constant (sum of P weights pi/P);
+    bins outside the detector read 0 (a detector narrower than the image leaves
+    the corners' far angles empty)."""
+    N, P = 32, 24
+    R = int(math.ceil(N * math.sqrt(2))) + 4
+    img = O.backproject_rtheta(np.full((P, R), 3.0), N)
+    assert np.allclose(img, 3.0 * math.pi, atol=1e-12)
+    img = O.backproject_rtheta(np.full((P, 9), 1.0), N)   # |r| <= 4 only
+    assert abs(img[N // 2, N // 2] - math.pi) < 1e-12
+    assert img[0, 0] < 0.5 * math.pi
+
+
+def test_ramp_filter_rtheta_zero_dc_and_spacing():
+    """Eq.7 taps sum to zero over the full band (sum_odd 1/n^2 = pi^2/8), so a long
+    constant row filters to ~0 in its interior; halving dr scales the kernel by
+    1/dr (h_dr(m) = h(m)/dr^2, times dr)."""
+    R = 401
+    q = O.ramp_filter_rtheta(np.ones((1, R)), dr=1.0, L0=4000)[0]
+    assert abs(q[R // 2]) < 2e-3            # tail beyond the row end: sum_{|m|>200} ~ 1/(pi^2 200)
+    x = np.random.default_rng(5).standard_normal((2, 64))
+    assert np.allclose(O.ramp_filter_rtheta(x, dr=0.5), 2.0 * O.ramp_filter_rtheta(x, dr=1.0),
+                       atol=1e-13)
+
+
+def _disc_sinogram(P, R, dr, rho, x0=0.0, y0=0.0):
+    """Closed-form chord lengths of a unit-density disc of radius rho centred at
+    (x0, y0) relative to the image centre: p(r, theta) = 2 sqrt(rho^2 - (r - x0 cos
+    - y0 sin)^2) (textbook; independent of the oracle)."""
+    th = np.arange(P) * math.pi / P
+    r = (np.arange(R) - 0.5 * (R - 1)) * dr
+    d = r[None, :] - (x0 * np.cos(th) + y0 * np.sin(th))[:, None]
+    return 2.0 * np.sqrt(np.clip(rho * rho - d * d, 0.0, None))
+
+
+@pytest.mark.parametrize("dr", [1.0, 0.5])
+def test_fbp_rtheta_recovers_disc(dr):
+    """FBP (Eq.3 + Eq.5) inverts the Radon transform: an off-centre unit disc is
+    recovered with density 1 inside and 0 outside (pins the |omega| kernel scale,
+    the 1/dr spacing, the pi/P half-turn weight and the centre/orientation: a
+    flipped theta or axis would move the disc)."""
+    N, P = 64, 128
+    R = int(math.ceil(N * math.sqrt(2) / dr)) + 8
+    x0, y0, rho = 9.0, -12.0, 10.0
+    img = O.fbp_rtheta(_disc_sinogram(P, R, dr, rho, x0, y0), N, dr)
+    c = np.arange(N) + 0.5 - N / 2.0
+    X, Y = np.meshgrid(c, c)
+    d = np.hypot(X - x0, Y - y0)
+    inside, outside = img[d < 0.8 * rho], img[(d > 1.3 * rho) & (np.hypot(X, Y) < N / 2 - 2)]
+    assert abs(inside.mean() - 1.0) < 0.01 and np.max(np.abs(inside - 1.0)) < 0.05
+    assert abs(outside.mean()) < 0.01 and np.max(np.abs(outside)) < 0.1   # edge streaks
+    # the mirrored disc position must NOT match (orientation pin)
+    dm = np.hypot(X - x0, Y + y0)
+    assert img[(dm < 0.5 * rho) & (d > 1.3 * rho)].mean() < 0.05
+
+
+def test_fbp_rtheta_recovers_ellipse_phantom():
+    """End to end on the phantom generator's analytic (r, theta) sinogram (textbook
+    ellipse projection, R23 geometry): best-fit scale 1 and a small RMSE
+    against the pixel-centre phantom (edges dominate the residual)."""
+    import phantoms
+    N, P = 64, 128
+    R = int(math.ceil(N * math.sqrt(2))) + 8
+    E = phantoms.draw_ellipses(N, 10, (6.0, 20.0), seed=41)
+    p = phantoms.sinogram_of_ellipses(E, N, P, R).numpy()
+    img = O.fbp_rtheta(p, N)
+    ref = phantoms.image_of_ellipses(E, N)
+    scale = float(np.sum(img * ref) / np.sum(ref * ref))
+    assert abs(scale - 1.0) < 0.03
+    assert np.sqrt(np.mean((img - ref) ** 2)) / np.sqrt(np.mean(ref ** 2)) < 0.2
