@@ -421,8 +421,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   const long long nitems = nsf * NB * nseg;
   // IIR roles: a quarter-warp = 8 rows x the same chunk (conflict-free), the TPR
   // chunks of a row sit 8 lanes apart in one warp.
+  // Step-1 row group of the thread Gt (rows 8Gt .. 8Gt+7): the IIR threads of a row
+  // group are its step-1 threads (no CTA barrier between F and step 1).
+  const int Gt = tid / (8 * TPR);
   const int iq = (tid >> 3) % TPR;
-  const int ir = (tid & 7) + 8 * (tid / (8 * TPR));
+  const int ir = (tid & 7) + 8 * Gt;
   const int lane = tid & 31;
   const unsigned long long pol_ef = policy_evict_first();
 
@@ -712,11 +715,14 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       if (back && !(dbgm & 1)) {
         // ---- FHT step 1 (levels 1-3): F -> S1 ----
         constexpr int NCH = X / C1;
-        const int jj = tid % NCH, G = tid / NCH;
+        static_assert(NCH == 8 * TPR, "step-1 row group = the IIR threads of its rows");
+        const int jj = tid % NCH, G = Gt;
         float2 v[8][It<3, C1>::T / 2];
         item_load<3, C1>(oF + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
         item_fht<3, C1>(v);
         const int gb = G & (NR2 - 1);                   // next step's block index
+        // outputs shifted by their step-2 pre-shift (r*gb) mod 4 (scalar stores: the
+        // aligned-store alternatives measured slower)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int o = oS + (G * 8 + r) * PS + HS + C1 * jj + ((r * gb) & 3);
@@ -787,7 +793,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       if (back) {
         constexpr int NCH = X / C1;                      // threads per step-1 row group
         using HG = HaloTabG<H, HS, O2, PS>;
-        const int G = tid / NCH, li = tid % NCH;
+        const int G = Gt, li = tid % NCH;
         const int cnt = kHaloTabG<H, HS, O2, PS>.cnt[G];
 #pragma unroll 2
         for (int i = li; i < cnt; i += NCH) {
@@ -865,6 +871,7 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
   constexpr int NR1 = 1 << R1, NR2 = 1 << R2;
   constexpr int C1 = (R1 == 3) ? 4 : 8;
   constexpr int C2 = (R2 == 3 || XB <= 64) ? 4 : 8;
+  constexpr bool DIRECT = (R2 == 2);                  // step 2 + epilogue in registers (no park)
   constexpr int O1 = It<R1, C1>::O, O2 = It<R2, C2>::O;
   constexpr int HS = pb_halo(R1, R2);
   constexpr int HI = HS + O1;
@@ -951,6 +958,7 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
         float2 v[NR1][It<R1, C1>::T / 2];
         item_load<R1, C1>(oIn + (q * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
         item_fht<R1, C1>(v);
+        // outputs shifted by their step-2 pre-shift (r*G) mod 4
 #pragma unroll
         for (int r = 0; r < NR1; ++r) {
           const int o = oS + (q * NB + G * NR1 + r) * PS + C1 * jj + ((r * G) & 3);
@@ -960,6 +968,62 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
       }
     }
     __syncthreads();
+    // ---- step 2, direct (radix-4 step 2): one thread per (channel row group c, column
+    //      item jj) runs the item of family 2p at jj and of family 2p+1 at the mirrored
+    //      item NCH2-1-jj, so the pair epilogue (mirror, add, weight) happens in
+    //      registers: pair 0 stores its NR2 image rows x C2 columns straight to HBM,
+    //      pair 1 its transposed 4x4 blocks into the reduce staging -- no park ----
+    if (DIRECT) {
+      constexpr int NCH2 = XB / C2;
+      if (!(dbgm & 1)) {
+        for (int it = tid; it < NR1 * NCH2; it += NT) {
+          // pair 0: jj fastest (coalesced image rows); pair 1: c fastest (the staging
+          // STS.128 of a warp spread over 8 bank quads)
+          const int c = PAIR == 0 ? it / NCH2 : it % NR1;
+          const int jj = PAIR == 0 ? it - c * NCH2 : it / NR1;
+          const int jm = NCH2 - 1 - jj;
+          float o[NR2][C2];
+          {
+            float2 v[NR2][It<R2, C2>::T / 2];
+            item_load<R2, C2>(oS + c * PS + HS + C2 * jj - O2, NR1 * PS, c, v);
+            item_fht<R2, C2>(v);
+#pragma unroll
+            for (int r = 0; r < NR2; ++r)
+#pragma unroll
+              for (int e = 0; e < C2; ++e) o[r][e] = col(v[r], O2 + e);
+          }
+          {
+            float2 v[NR2][It<R2, C2>::T / 2];
+            item_load<R2, C2>(oS + (NB + c) * PS + HS + C2 * jm - O2, NR1 * PS, c, v);
+            item_fht<R2, C2>(v);
+            // column C2*jj + e of family 2p+1 mirrored: XB-1-(C2*jj+e) = C2*jm + C2-1-e
+#pragma unroll
+            for (int r = 0; r < NR2; ++r)
+#pragma unroll
+              for (int e = 0; e < C2; ++e) o[r][e] = scale * (o[r][e] + col(v[r], O2 + C2 - 1 - e));
+          }
+          if (dbgm & 2) continue;
+          if (PAIR == 0) {
+            // img[ch*NB + c*NR2 + r][x0 + C2*jj + e]
+            float* const outc = img + ((long long)cur.sl * N + ch * NB + c * NR2) * N + x0 + C2 * jj;
+            if (x0 + C2 * jj < N) {
+#pragma unroll
+              for (int r = 0; r < NR2; ++r)
+#pragma unroll
+                for (int e = 0; e < C2; e += 4)
+                  *reinterpret_cast<float4*>(outc + (long long)r * N + e) =
+                      make_float4(o[r][e], o[r][e + 1], o[r][e + 2], o[r][e + 3]);
+            }
+          } else {
+            // staging [XB image rows x0 + i][NB image columns ch*NB + r], i = C2*jj + e
+#pragma unroll
+            for (int e = 0; e < C2; ++e)
+              st4(oIn + oStg + (C2 * jj + e) * NB + c * NR2, make_float4(o[0][e], o[1][e], o[2][e], o[3][e]));
+          }
+        }
+      }
+      if (PAIR == 1) fence_proxy_async();              // staging -> async proxy (each writer)
+    } else {
     // ---- step 2: both families, core columns -> park (aliasing the input) ----
     if (!(dbgm & 1)) {
       constexpr int nch = XB / C2;
@@ -1018,7 +1082,8 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
       }
       fence_proxy_async();                             // staging -> async proxy (each writer)
     }
-    __syncthreads();                                   // park / staging reused by the next item
+    }   // !DIRECT
+    __syncthreads();                                   // S1 / park / staging reused by the next item
     // pair 1: image[x0 + i][ch*NB + r] += staging (TMA reduce in L2; clipped at row N)
     if (PAIR == 1 && tid == 0 && !(dbgm & 2))
       tma_reduce_add_2d(&tmapI, smem_u32(oIn + oStg), ch * NB, cur.sl * N + x0);
