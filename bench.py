@@ -558,7 +558,8 @@ def run_fbp(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 200; --impl reference: 10, each step ~2 s of oracle work)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=16, help="slices per GPU per step")
     ap.add_argument("--n", type=int, default=N_HEADLINE)
@@ -572,6 +573,8 @@ def main():
     ap.add_argument("--no-gather", action="store_true")
     ap.add_argument("--no-forward", action="store_true", help="skip the NEXT-1/NEXT-2 line items (forward FHT, resampling)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if args.impl == "reference" else 200
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -4,6 +4,7 @@
 #include "fbp_internal.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: host ranges per entry point and kernel
 
 #include <algorithm>
 #include <cmath>
@@ -161,8 +162,18 @@ cudaEvent_t pool_get(const fbp_plan* p) {
 }
 
 // Run one kernel launcher; when profiling, bracket it with events on its stream.
+// RAII NVTX range (host timeline of each entry point and kernel launch; no cost
+// without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename Fn>
 cudaError_t timed(const fbp_plan* p, int kind, cudaStream_t st, Fn&& fn) {
+  static const char* const kNames[] = {"fbp:iir", "fbp:fht_pass_a", "fbp:fht_pass_b", "fbp:fwd_pass_a",
+                                       "fbp:fwd_pass_b", "fbp:resample"};
+  NvtxRange range(kind >= 0 && kind < 6 ? kNames[kind] : "fbp:kernel");
   if (!p->profiling) return fn();
   cudaEvent_t a = pool_get(p), b = pool_get(p);
   cudaEventRecord(a, st);
@@ -500,6 +511,7 @@ void fbp_plan_destroy(fbp_plan* p) {
 
 fbp_status fbp_iir_filter(const fbp_plan* p, const float* sino, float* filtered, int batch,
                           void* stream) {
+  NvtxRange nvtx_range("fbp_iir_filter");
   fbp_status s = check_call(p, sino, filtered, batch);
   if (s != FBP_OK || batch == 0) return s;
   DeviceGuard guard(p->device);
@@ -515,6 +527,7 @@ fbp_status fbp_iir_filter(const fbp_plan* p, const float* sino, float* filtered,
 
 fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image, int batch,
                                float scale, void* stream) {
+  NvtxRange nvtx_range("fbp_fht_backproject");
   fbp_status s = check_call(p, lin, image, batch);
   if (s != FBP_OK || batch == 0) return s;
   DeviceGuard guard(p->device);
@@ -541,6 +554,7 @@ fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image
 }
 
 fbp_status fbp_fht_forward(const fbp_plan* p, const float* image, float* lin, int batch, void* stream) {
+  NvtxRange nvtx_range("fbp_fht_forward");
   fbp_status s = check_call(p, image, lin, batch);
   if (s != FBP_OK || batch == 0) return s;
   DeviceGuard guard(p->device);
@@ -569,6 +583,7 @@ fbp_status fbp_fht_forward(const fbp_plan* p, const float* image, float* lin, in
 
 fbp_status fbp_resample_sinogram(const fbp_plan* p, const float* sino, int n_angles, int n_bins, double dr,
                                  float* lin, int batch, void* stream) {
+  NvtxRange nvtx_range("fbp_resample_sinogram");
   fbp_status s = check_call(p, sino, lin, batch);
   if (s != FBP_OK || batch == 0) return s;
   if (n_angles < 1 || n_bins < 1) return fail(FBP_ERR_PARAM, "n_angles and n_bins must be >= 1");
@@ -595,6 +610,7 @@ fbp_status fbp_resample_sinogram(const fbp_plan* p, const float* sino, int n_ang
 
 fbp_status fbp_reconstruct(const fbp_plan* p, const float* sino, float* image, int batch,
                            void* stream) {
+  NvtxRange nvtx_range("fbp_reconstruct");
   fbp_status s = check_call(p, sino, image, batch);
   if (s != FBP_OK || batch == 0) return s;
   DeviceGuard guard(p->device);
@@ -606,6 +622,7 @@ fbp_status fbp_reconstruct(const fbp_plan* p, const float* sino, float* image, i
 }
 
 fbp_status fbp_reconstruct_host(const fbp_plan* cp, const float* sino, float* image, int batch) {
+  NvtxRange nvtx_range("fbp_reconstruct_host");
   if (!cp) return fail(FBP_ERR_PARAM, "plan is NULL");
   if (batch < 0) return fail(FBP_ERR_PARAM, "batch < 0");
   if (batch == 0) return FBP_OK;

@@ -47,6 +47,14 @@
 // steps / epilogue to attribute time) -- compiled in only with -DFBP_DEV_MASK=1
 // (fbp_internal.h).
 
+#ifndef FBP_KS_PFD
+#define FBP_KS_PFD 2   // sweep: TMA L2 prefetch distance in tiles (measured: 1-2 best, 4 +1 %, 8 +3 %)
+#endif
+
+#ifndef FBP_KB_SKIP
+#define FBP_KB_SKIP 1   // pass B step 1: skip halo items no step-2 pre-shift reads
+#endif
+
 namespace fbp {
 
 namespace {
@@ -478,7 +486,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     };
     // L2 prefetch of raw tile jt (TMA, no shared memory): the landing of a tile is
     // issued one step ahead, its first touch of HBM PF tiles ahead
-    constexpr int PFD = 4;
+    constexpr int PFD = FBP_KS_PFD;
     auto prefetch = [&](int jt) {
       if (tid == 0 && jt < nt && !(dbgm & 8)) tma_prefetch_2d(&tmapF, jt * X - 8, trow);
     };
@@ -679,14 +687,15 @@ __global__ void __launch_bounds__(H * X / 32, 3)
               tm[2] = acc[2];
             }
           }
+          const int slot_j = slot_t == D ? 0 : slot_t + 1;   // slot of tile j = t - D
           float P[32];
           tmem_wait_st();
-          tmem_ld32(tbase + 32u * (slot_t == D ? 0 : slot_t + 1), P);   // slot of tile j = t - D
+          tmem_ld32(tbase + 32u * slot_j, P);
+          const int rowF = oF + ir * PF + HF + 32 * iq;
           // homogeneous anticausal response at sample i: sum_m (A^(32-i))_{0m} tm_m,
           // adjacent samples packed (plan table k.GA)
           const float2 t0 = make_float2(tm[0], tm[0]), t1 = make_float2(tm[1], tm[1]),
                        t2 = make_float2(tm[2], tm[2]);
-          const int rowF = oF + ir * PF + HF + 32 * iq;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float2 a = make_float2(P[4 * q], P[4 * q + 1]);
@@ -861,6 +870,20 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// First pass-B step-1 item (of C1 columns) of row group G that step 2 reads: the
+// step-2 windows of row (G, r) start at virtual column HS - O2 - r*G (pre-shift r*G,
+// r < 2^R1), so the items entirely left of HS - O2 - (2^R1 - 1)*G are never read.
+template <int R1, int C1, int HS, int O2>
+__host__ __device__ constexpr int pb_js(int G) {
+  return (HS - O2 - ((1 << R1) - 1) * G) > 0 ? (HS - O2 - ((1 << R1) - 1) * G) / C1 : 0;
+}
+template <int R1, int C1, int HS, int O2, int NGF>
+__host__ __device__ constexpr int pb_items(int nch) {
+  int n = 0;
+  for (int G = 0; G < NGF; ++G) n += nch - pb_js<R1, C1, HS, O2>(G);
+  return n;
+}
+
 template <int R1, int R2, int XB, int PAIR, bool DB>
 __global__ void __launch_bounds__(256, DB ? 3 : 2)
     k_pair_b(const float* __restrict__ Rin, float* __restrict__ img, SweepGeom g, float scale,
@@ -950,11 +973,35 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
     // ---- step 1: both families, output virtual cols [0, HS + XB) ----
     if (!(dbgm & 1)) {
       constexpr int nch = (HS + XB) / C1;
-      constexpr int per_fam = (NB / NR1) * nch;
+      constexpr int NGF = NB / NR1;                    // row groups per family
+#if FBP_KB_SKIP
+      // the items of group G left of pb_js(G) (halo columns no step-2 pre-shift
+      // reaches) are skipped
+      constexpr int per_fam = pb_items<R1, C1, HS, O2, NGF>(nch);
+#else
+      constexpr int per_fam = NGF * nch;
+#endif
       for (int it = tid; it < 2 * per_fam; it += NT) {
         const int q = it / per_fam;
         const int r3 = it - q * per_fam;
+#if FBP_KB_SKIP
+        int G = 0, rem = r3;
+#pragma unroll
+        for (int gg = 0; gg + 1 < NGF; ++gg) {
+          const int cnt = nch - pb_js<R1, C1, HS, O2>(gg);
+          if (G == gg && rem >= cnt) {
+            rem -= cnt;
+            G = gg + 1;
+          }
+        }
+        int js = 0;
+#pragma unroll
+        for (int gg = 0; gg < NGF; ++gg)
+          if (G == gg) js = pb_js<R1, C1, HS, O2>(gg);
+        const int jj = js + rem;
+#else
         const int G = r3 / nch, jj = r3 - G * nch;
+#endif
         float2 v[NR1][It<R1, C1>::T / 2];
         item_load<R1, C1>(oIn + (q * NB + G * NR1) * PI + C1 * jj, PI, 0, v);
         item_fht<R1, C1>(v);

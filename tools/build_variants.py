@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Build libfbp.so variants that differ in sweep.cu compile-time switches (A/B
+"""Build libfbp.so variants that differ in compile-time switches (A/B
 measurement on one GPU call).  Output: paper_2007_06289_b200/variants/<name>.so.
 
     python tools/build_variants.py name1:-DFOO=1,-DBAR=0 name2:-DFOO=0 ...
@@ -31,19 +31,19 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     variants = [(a.split(":")[0], [f for f in a.split(":")[1].split(",") if f]) for a in sys.argv[1:]]
     srcs = B.sources()
-    sweep = [s for s in srcs if s.endswith("sweep.cu")][0]
-    others = [s for s in srcs if s != sweep]
-    with cf.ThreadPoolExecutor(8) as ex:
-        common = list(ex.map(lambda s: cc(s, os.path.join(OUT, os.path.basename(s) + ".o"), []), others))
-        vobj = list(ex.map(lambda v: cc(sweep, os.path.join(OUT, f"sweep_{v[0]}.o"), v[1]), variants))
-    for (name, _), o in zip(variants, vobj):
+    jobs = [(v, src) for v in variants for src in srcs]
+    with cf.ThreadPoolExecutor(12) as ex:
+        objs = list(ex.map(lambda j: cc(j[1], os.path.join(OUT, f"{j[0][0]}_{os.path.basename(j[1])}.o"), j[0][1]),
+                           jobs))
+    for name, _ in variants:
+        mine = [o for (v, _), o in zip(jobs, objs) if v[0] == name]
         so = os.path.join(OUT, f"{name}.so")
-        r = subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", so, o] + common +
+        r = subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", so] + mine +
                            ["-lcudart_static", "-lrt", "-ldl", "-lpthread"], capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(r.stderr)
         print(so)
-    for o in common + vobj:
+    for o in objs:
         os.remove(o)
 
 

@@ -10,6 +10,8 @@ for v in ${VARIANTS}; do
   timeout 300 python bench.py --steps 50 --no-cpu-baseline --no-e2e --no-variants ${BENCH_ARGS:---no-forward} > gpurun_out/ab_bench_$v.log 2>&1
   tail -1 gpurun_out/ab_bench_$v.log | python -c "
 import json,sys; d=json.loads(sys.stdin.read())
-print('  $v value', round(d['value'],1), 'ms', round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['kernel_ms_per_step'].items() if v}, d['clocks']['sm_mhz'])" 2>&1
+print('  $v value', round(d['value'],1), 'ms', round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['kernel_ms_per_step'].items() if v}, d['clocks']['sm_mhz'])
+f=d.get('next',{}).get('fht_forward')
+f and print('  $v fwd', round(f['value'],1), round(f['ms_per_step'],4), f['kernel_ms_per_step'], 'frac', round(f['roofline']['frac'],3))" 2>&1
 done
 cp /tmp/libfbp_default.so paper_2007_06289_b200/libfbp.so
