@@ -19,6 +19,13 @@
 
 #include "fbp_internal.h"
 
+#ifndef FBP_FWD_FX6
+#define FBP_FWD_FX6 192   // item-path tile width (output columns per CTA), 64-row passes (128, 160: +9 %, 256: +4 %)
+#endif
+#ifndef FBP_FWD_FX5
+#define FBP_FWD_FX5 384   // the same, 32-row passes (measured: 320 +2 %, 448 +9 %, 576 +14 % pass-B time)
+#endif
+
 namespace fbp {
 namespace {
 
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(FNT2) k_fwd_item(const float* __restrict__ src
 // tile widths (output columns per CTA), ~64-72 KB of shared memory: 3 CTAs/SM
 template <int R1, int R2>
 struct FwdFX {
-  static constexpr int value = (R1 + R2 == 6) ? 192 : (R1 + R2 == 5) ? 448 : 960;
+  static constexpr int value = (R1 + R2 == 6) ? FBP_FWD_FX6 : (R1 + R2 == 5) ? FBP_FWD_FX5 : 960;
 };
 
 template <int R1, int R2, int MODE>

@@ -40,6 +40,18 @@ for N in [int(a) for a in (sys.argv[1:] or ["512", "1024", "2048", "4096"])]:
         ok &= good
         print(f"N={N} B={B} {v}: int BP bit-equal {ex}, recon max rel diff {err:.2e} {'OK' if good else 'FAIL'}",
               flush=True)
+        if v == "dc0":
+            # forward FHT (NEXT-1) by the exact adjoint identity <fwd(img), P> = <img, BP(P)>
+            # on small integers, BP from the general path
+            img = P.integer_image(N, 2, seed=N + 2, lo=-15, hi=15).cuda()
+            Li = P.integer_linogram(N, 2, seed=N + 3, lo=-15, hi=15).cuda()
+            fw = fast.forward(img).double()
+            bp = gen.backproject(Li, scale=1.0).double()
+            lhs = float((fw * Li.double()).sum())
+            rhs = float((img.double() * bp).sum())
+            adj = lhs == rhs
+            ok &= adj
+            print(f"N={N} forward adjoint identity exact {adj} ({lhs:.0f} vs {rhs:.0f})", flush=True)
         fast.close()
         gen.close()
 print("ALL OK" if ok else "FAILURES")
