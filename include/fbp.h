@@ -140,7 +140,10 @@ FBP_API fbp_status fbp_resample_sinogram(const fbp_plan* plan, const float* sino
  * next D tiles only, and a sweep (or sweep segment) starts its causal recursion
  * from zero state D tiles before the first tile it needs.  D is the smallest tile
  * count whose dropped impulse-response tail is <= 1e-9 of its l1 norm
- * (reading R22).  The general path's recursions are exact.
+ * (reading R22).  The general path's recursions are exact, and so
+ * are those of the small-N path (N <= 64 with M, Q <= 3: one CTA per slice runs
+ * both recursions over whole rows, every FHT level and the Eq.22 sum on-chip;
+ * fbp_fht_backproject uses the same kernel without the IIR for any M, Q).
  */
 FBP_API fbp_status fbp_reconstruct(const fbp_plan* plan, const float* sino, float* image, int batch,
                            void* cuda_stream);
@@ -171,9 +174,10 @@ FBP_API long long fbp_plan_launch_count(const fbp_plan* plan);
  * every kernel while enabled).  fbp_plan_profile(plan, 1) clears and enables,
  * 0 disables.  fbp_plan_kernel_times synchronises on the recorded events and
  * writes, for kind k in {0: IIR, 1: FHT pass A, 2: FHT pass B, 3: forward FHT
- * pass A, 4: forward FHT pass B, 5: sinogram resampling}, the summed milliseconds
- * ms[k] and launch count launches[k] (arrays of length `kinds`, at most 6) since
- * the last enable, then clears the record.
+ * pass A, 4: forward FHT pass B, 5: sinogram resampling, 6: small-N slice kernel
+ * (N <= 64: IIR + FHT + Eq.22 in one kernel)}, the summed milliseconds ms[k] and
+ * launch count launches[k] (arrays of length `kinds`, at most 7) since the last
+ * enable, then clears the record.
  */
 FBP_API fbp_status fbp_plan_profile(fbp_plan* plan, int enable);
 FBP_API fbp_status fbp_plan_kernel_times(fbp_plan* plan, double* ms, long long* launches, int kinds);

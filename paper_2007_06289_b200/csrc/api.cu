@@ -36,6 +36,9 @@ struct fbp_plan {
   float* h_in[2] = {nullptr, nullptr};
   float* h_out[2] = {nullptr, nullptr};
   cudaStream_t s_copy = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  // small-N path (small.cu): N <= 64, one CTA per slice; the IIR part needs M, Q <= 3
+  bool small = false, small_iir = false;
+  SmallIir sk{};
   // fast path (sweep.cu): fused IIR + pass-A sweep and pair-wise pass B
   bool fast = false;
   SweepGeom sg{};
@@ -172,8 +175,8 @@ struct NvtxRange {
 template <typename Fn>
 cudaError_t timed(const fbp_plan* p, int kind, cudaStream_t st, Fn&& fn) {
   static const char* const kNames[] = {"fbp:iir", "fbp:fht_pass_a", "fbp:fht_pass_b", "fbp:fwd_pass_a",
-                                       "fbp:fwd_pass_b", "fbp:resample"};
-  NvtxRange range(kind >= 0 && kind < 6 ? kNames[kind] : "fbp:kernel");
+                                       "fbp:fwd_pass_b", "fbp:resample", "fbp:small"};
+  NvtxRange range(kind >= 0 && kind < 7 ? kNames[kind] : "fbp:kernel");
   if (!p->profiling) return fn();
   cudaEvent_t a = pool_get(p), b = pool_get(p);
   cudaEventRecord(a, st);
@@ -227,6 +230,8 @@ cudaError_t run_reconstruct(const fbp_plan* p, const float* sino, float* img, in
   const float w = 1.0f / (float)g.N;  // exact power of two (R7)
   const long long fam_elems = (long long)g.N * g.W;
   if (p->fast) return run_fast(p, sino, img, batch, w, true, st, launches);
+  if (p->small_iir)
+    return timed(p, 6, st, [&] { return launch_small(sino, img, batch, p->sk, w, st, launches); });
   if (p->per_family) {
     // Large N: one line family at a time, so that the filtered family (N x 2N
     // fp32, 32 MiB at N = 2048) is consumed by pass A while it is L2-resident;
@@ -444,6 +449,23 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
     }
   }
 
+  // ---- small-N path (N <= 64): one CTA per slice, everything on-chip ----
+  if (small_supported(n)) {
+    p->small = true;
+    p->small_iir = (m <= 3 && q <= 3);
+    double bb[3] = {0, 0, 0}, aa[3] = {0, 0, 0};
+    for (int i = 0; i < m && i < 3; ++i) bb[i] = b[i];
+    for (int i = 0; i < q && i < 3; ++i) aa[i] = a[i];
+    p->sk.N = n;
+    p->sk.iir = 1;
+    p->sk.beta = (float)(bb[0] + bb[1] + bb[2]);   // difference form (R16): beta + (1 - z^-1) C(z)
+    p->sk.c0 = (float)(-(bb[1] + bb[2]));
+    p->sk.c1 = (float)(-bb[2]);
+    p->sk.na1 = (float)(-aa[0]);
+    p->sk.na2 = (float)(-aa[1]);
+    p->sk.na3 = (float)(-aa[2]);
+  }
+
   // ---- workspace, sized for a group of slices ----
   const Geometry& g = p->g;
   const size_t f_slice = p->fast ? 0 : (size_t)4 * g.N * g.W * sizeof(float);
@@ -536,6 +558,15 @@ fbp_status fbp_fht_backproject(const fbp_plan* p, const float* lin, float* image
   const long long img_elems = (long long)p->g.N * p->g.N;
   if (p->fast) {
     cudaError_t e = run_fast(p, lin, image, batch, scale, false, (cudaStream_t)stream, &launches);
+    p->launches = launches;
+    if (e != cudaSuccess) return cuda_fail(e, "fbp_fht_backproject");
+    return FBP_OK;
+  }
+  if (p->small) {
+    SmallIir k = p->sk;
+    k.iir = 0;
+    cudaError_t e = timed(p, 6, (cudaStream_t)stream,
+                          [&] { return launch_small(lin, image, batch, k, scale, (cudaStream_t)stream, &launches); });
     p->launches = launches;
     if (e != cudaSuccess) return cuda_fail(e, "fbp_fht_backproject");
     return FBP_OK;
@@ -754,7 +785,7 @@ fbp_status fbp_plan_profile(fbp_plan* p, int enable) {
 }
 
 fbp_status fbp_plan_kernel_times(fbp_plan* p, double* ms, long long* launches, int kinds) {
-  if (!p || kinds < 0 || kinds > 6 || (kinds > 0 && (!ms || !launches)))
+  if (!p || kinds < 0 || kinds > 7 || (kinds > 0 && (!ms || !launches)))
     return fail(FBP_ERR_PARAM, "fbp_plan_kernel_times: bad arguments");
   DeviceGuard guard(p->device);
   for (int k = 0; k < kinds; ++k) {

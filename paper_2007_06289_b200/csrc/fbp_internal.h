@@ -94,6 +94,17 @@ cudaError_t launch_sweep_a(const float* lin, float* R, int slices, int f0, int n
 cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, float scale,
                           const SweepGeom& g, cudaStream_t st, int* launches);
 bool sweep_supported(int N);
+
+// Small-N path (small.cu, N <= 64): one CTA per slice, IIR + FHT + Eq.22 on-chip.
+struct SmallIir {
+  int N;
+  int iir;                     // 0: back projection only (fbp_fht_backproject)
+  float beta, c0, c1;          // difference-form feedforward (M <= 3)
+  float na1, na2, na3;         // -a_1, -a_2, -a_3 (Q <= 3)
+};
+bool small_supported(int N);
+cudaError_t launch_small(const float* lin, float* img, int slices, const SmallIir& k, float scale, cudaStream_t st,
+                         int* launches);
 size_t sweep_a_smem(const SweepGeom& g);
 size_t pair_b_smem(const SweepGeom& g, int pair);
 

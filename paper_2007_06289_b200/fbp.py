@@ -30,7 +30,7 @@ EXPORTED = ["fbp_plan_create", "fbp_plan_destroy", "fbp_iir_filter", "fbp_fht_ba
             "fbp_plan_launch_count", "fbp_plan_info", "fbp_plan_path", "fbp_plan_profile",
             "fbp_plan_kernel_times"]
 
-KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b", "fwd_pass_a", "fwd_pass_b", "resample")
+KERNEL_KINDS = ("iir", "fht_pass_a", "fht_pass_b", "fwd_pass_a", "fwd_pass_b", "resample", "small")
 
 
 class FbpError(RuntimeError):
