@@ -596,3 +596,35 @@ def test_determinism_stress_bench_config(fbp):
             want = (O.backproject_pixel(Li, 0, y, x) + O.backproject_pixel(Li, 1, y, N - 1 - x)
                     + O.backproject_pixel(Li, 2, x, y) + O.backproject_pixel(Li, 3, x, N - 1 - y))
             assert float(bp[i, y, x]) == want, (i, y, x)
+
+
+# ------------------------------------------------------- small-N path (N <= 64)
+@pytest.mark.parametrize("N,variant", [(2, "dc0"), (4, "spec"), (8, "dc0"), (16, "spec"), (64, "spec")])
+def test_small_path_all_sizes(fbp, N, variant):
+    """The one-CTA-per-slice kernel (small.cu) at every N it serves, both coefficient
+    sets (spec: beta != 0), random inputs vs the oracle reconstruction (1e-4 of the
+    slice peak; its recursions are exact, reading R16/R11)."""
+    b, a = coeffs(N, variant)
+    plan = fbp.Plan(N, b, a, max_batch=3)
+    S = P.random_linogram(N, 3, seed=900 + N, scale=20.0)
+    img = plan.reconstruct(S.cuda()).cpu().numpy()
+    for i in range(3):
+        assert rel_err(img[i], O.reconstruct(S[i].double().numpy(), b, a)) < TOL, (N, i)
+
+
+def test_small_path_persistent_batch(fbp):
+    """More slices than resident CTAs (N = 64: 2 per SM, 300 > 296): every CTA loops
+    over slices with double-buffered family landings; sampled slices vs the oracle,
+    integer back projections of the same batch bit-exact."""
+    N, B = 64, 300
+    b, a = coeffs(N)
+    plan = fbp.Plan(N, b, a, max_batch=B)
+    S = P.random_linogram(N, B, seed=77, scale=20.0)
+    img = plan.reconstruct(S.cuda()).cpu().numpy()
+    for i in (0, 1, 149, 295, 296, 299):
+        assert rel_err(img[i], O.reconstruct(S[i].double().numpy(), b, a)) < TOL, i
+    L = P.integer_linogram(N, B, seed=78)
+    bp = plan.backproject(L.cuda(), scale=1.0).cpu().numpy()
+    for i in (0, 150, 296, 299):
+        ref = O.combine(O.fht_backproject(L[i].double().numpy()), 1.0)
+        assert np.array_equal(bp[i].astype(np.float64), ref), i
