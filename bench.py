@@ -203,6 +203,22 @@ def ncu_traffic(kind: str):
     return v.get("dram_bytes_per_slice"), v.get("source")
 
 
+def path_dram(B: int, ms_step: float, world: int, peak: float):
+    """ncu DRAM bytes per slice summed over the path's kernel kinds (profiles/
+    ncu_traffic.json) x slices per step / live step time: SURVEY 8(d)'s ncu-achieved
+    DRAM bandwidth, as a fraction of the measured peak and of 6557 / 8000 GB/s."""
+    tot, src = 0.0, None
+    for kind in ("fht_pass_a", "fht_pass_b"):
+        b, s = ncu_traffic(kind)
+        if b is None:
+            return None
+        tot += b
+        src = s
+    gbs = tot * B / (ms_step / 1e3) / 1e9
+    return {"bytes_per_slice": tot, "achieved": gbs, "frac": gbs / peak, "frac_6557": gbs / 6557.0,
+            "frac_8000": gbs / 8000.0, "unit": "GB/s per GPU", "source": src}
+
+
 # ------------------------------------------------------- CPU oracle pool
 _POOL_DATA = {}
 
@@ -525,7 +541,10 @@ def run_fbp(args):
             "path_roofline": {"alg_bytes_per_slice": alg_bytes_per_slice(N),
                               "achieved": path_bytes / (ms_clean / 1e3) / 1e9 / world,
                               "frac": path_bytes / (ms_clean / 1e3) / 1e9 / world / peak,
-                              "unit": "GB/s per GPU"},
+                              "unit": "GB/s per GPU",
+                              # SURVEY 8(d)'s other figure: ncu DRAM bytes of all kernels of
+                              # one call (committed bench-batch capture) over the live step time
+                              "ncu_dram": path_dram(B, ms_clean, world, peak)},
             "kernel_share": shares,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
             "gpu_launches": launches[0],

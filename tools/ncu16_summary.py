@@ -52,6 +52,14 @@ for key in order:
     t = traffic.setdefault(kind, {"dram_bytes_per_slice": 0.0, "launches": 0})
     t["dram_bytes_per_slice"] += (rd + wr) / slices
     t["launches"] += 1
+# whole path: ncu DRAM bytes over all kernels of one call / summed kernel time
+tb = sum(k[key].get("dram__bytes_read.sum", 0) + k[key].get("dram__bytes_write.sum", 0) for key in order)
+tt = sum(k[key].get("gpu__time_duration.sum", 0) for key in order) * 1e-9
+if tt > 0:
+    gbs = tb / tt / 1e9
+    lines += ["", f"Whole path (all {len(order)} launches of one call): {tb / slices / 1e6:.1f} MB DRAM per slice, "
+              f"{gbs:.0f} GB/s = {gbs / 6557:.3f} of 6557 GB/s (measured copy, SURVEY) / {gbs / 8000:.3f} of 8000 GB/s "
+              f"(spec); algorithmic 36 N^2 = {36 * 2048 * 2048 / 1e6:.1f} MB per slice"]
 for kind, t in traffic.items():
     t["source"] = os.path.basename(dst)
     t["batch"] = slices
