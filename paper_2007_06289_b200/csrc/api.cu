@@ -12,10 +12,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
-
-#ifndef FBP_KB_CHUNK
-#define FBP_KB_CHUNK 0   // pass-B slices per launch pair (0: the whole sweep group)
-#endif
 #include <string>
 #include <vector>
 
@@ -216,19 +212,11 @@ cudaError_t run_fast(const fbp_plan* p, const float* lin, float* img, int batch,
                             p->counter, st, launches);
     });
     if (e != cudaSuccess) return e;
-    // pass B in chunks of FBP_KB_CHUNK slices (0: the whole group): pair 1 adds into
-    // image rows pair 0 has just written, while they are still L2-resident
-    const int kc = FBP_KB_CHUNK > 0 ? FBP_KB_CHUNK : ns;
-    const long long r_elems = 4LL * p->sg.H * p->sg.NB * p->sg.WR;   // compact R per slice
-    for (int c0 = 0; c0 < ns; c0 += kc) {
-      const int nc = std::min(kc, ns - c0);
-      for (int pair = 0; pair < 2; ++pair) {
-        e = timed(p, 2, st, [&] {
-          return launch_pair_b(p->R + c0 * r_elems, img + (s0 + c0) * img_elems, nc, pair, scale, p->sg, st,
-                               launches);
-        });
-        if (e != cudaSuccess) return e;
-      }
+    for (int pair = 0; pair < 2; ++pair) {
+      e = timed(p, 2, st, [&] {
+        return launch_pair_b(p->R, img + s0 * img_elems, ns, pair, scale, p->sg, st, launches);
+      });
+      if (e != cudaSuccess) return e;
     }
   }
   return cudaSuccess;

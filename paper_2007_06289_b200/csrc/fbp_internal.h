@@ -105,7 +105,7 @@ struct SmallIir {
 bool small_supported(int N);
 cudaError_t launch_small(const float* lin, float* img, int slices, const SmallIir& k, float scale, cudaStream_t st,
                          int* launches);
-size_t sweep_a_smem(const SweepGeom& g, bool iir);
+size_t sweep_a_smem(const SweepGeom& g);
 size_t pair_b_smem(const SweepGeom& g, int pair);
 
 // Kernel launchers of the general path (iir.cu, fht.cu).  All asynchronous on `st`; return the launch error.

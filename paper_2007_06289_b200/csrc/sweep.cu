@@ -51,14 +51,6 @@
 #define FBP_KS_PFD 2   // sweep: TMA L2 prefetch distance in tiles (measured: 1-2 best, 4 +1 %, 8 +3 %)
 #endif
 
-#ifndef FBP_KS_DBUF
-#define FBP_KS_DBUF 1   // sweep (IIR): two tile buffers, raw tile t+2 lands while t+1 is in flight
-#endif
-
-#ifndef FBP_KB_EF
-#define FBP_KB_EF 0     // pass B: evict-first L2 hint on the R box loads
-#endif
-
 #ifndef FBP_KB_SKIP
 #define FBP_KB_SKIP 1   // pass B step 1: skip halo items no step-2 pre-shift reads
 #endif
@@ -122,15 +114,6 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
       ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-// the same with an L2 cache-policy hint (e.g. evict-first for data read once)
-__device__ __forceinline__ void tma_load_3d_hint(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                                 unsigned bar, unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
-      ::"r"(dst), "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
 // L2 prefetch of a tensor box (no shared memory, no completion tracking)
@@ -302,11 +285,9 @@ __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, flo
 // ===========================================================================
 // Pass A sweep.  Threads NT = H*X/32 = 128 (thread = one 32-sample chunk of a row
 // in the IIR, one register item in the FHT steps).  Shared memory (floats):
-//   F      : NFB x H x PF  landing target of raw tile t (TMA box, columns tX-8 ..
+//   F      : H x PF  landing target of raw tile t (TMA box, columns tX-8 ..
 //            tX+X+4) and, once the IIR has read it, the filtered tile F(t-D):
-//            halo [0, HF) = F(t-D-1)'s last HF columns, core [HF, HF+X).  IIR
-//            sweeps alternate two buffers (NFB = 2): tile t+2 lands while the
-//            iteration of tile t+1 runs, a whole iteration of TMA latency hidden
+//            halo [0, HF) = F(t-D-1)'s last HF columns, core [HF, HF+X)
 //   stash  : H x HF  the core's last HF columns (halo of the next F tile)
 //   S1     : H x PS  step-1 output, core [HS, HS+X), halo [0, HS)
 //   ring   : (D+1) x H x 3  anticausal tile aggregates agg[t]
@@ -416,27 +397,23 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);   // step-2 input halo
   constexpr int PF = pitch4(HF + X + 4);
   constexpr int PS = pitch4(HS + X + 4);
-  // IIR sweeps alternate two tile buffers (raw tile t lands in buffer (t - jst) & 1,
-  // F(t - D) overwrites it after the front, step 1 reads it); the fast FHT-only sweep
-  // lands F itself into one buffer
-  constexpr int NFB = (IIR && FBP_KS_DBUF) ? 2 : 1;
-  constexpr int oStash = NFB * H * PF, oS = oStash + H * HF, oRing = oS + H * PS;
+  constexpr int oF = 0, oStash = H * PF, oS = oStash + H * HF, oRing = oS + H * PS;
   static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
   static_assert(NT == 128, "TMEM lanes: one per thread");
 
   const int tid = threadIdx.x;
   const int D = IIR ? g.D : 0;
   const int dbgm = FBP_DEV_MASK ? g.dbg : 0;
-  // NFB mbarriers (tile landings), the work item, the TMEM base address
+  // 1 mbarrier (F landing), the work item, the TMEM base address
   const int oBar = (oRing + (D + 1) * H * 3 + 3) & ~1;
-  int* s_item = reinterpret_cast<int*>(sm + oBar + 2 * NFB);
-  unsigned* s_tmem = reinterpret_cast<unsigned*>(sm + oBar + 2 * NFB + 1);
+  int* s_item = reinterpret_cast<int*>(sm + oBar + 2);
+  unsigned* s_tmem = reinterpret_cast<unsigned*>(sm + oBar + 3);
   if (tid == 0) {
-    for (int i = 0; i < NFB; ++i) mbar_init(smem_u32(oBar + 2 * i), 1);
+    mbar_init(smem_u32(oBar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (IIR && tid < 32) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(oBar + 2 * NFB + 1)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(oBar + 3)),
                  "r"(g.tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
@@ -446,7 +423,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   // this thread's TMEM lane: warp w owns lanes 32w .. 32w + 31
   const unsigned tbase = IIR ? (*s_tmem + ((unsigned)(tid & ~31) << 16)) : 0u;
-  unsigned ph = 0;                                       // phase bits of the mbarriers (bit i: buffer i)
+  unsigned ph = 0;                                       // phase bit of the mbarrier
   const int N = g.N, W = g.W, NB = g.NB, nt = g.nt;
   const long long nsf = (long long)slices * nf;
   const long long nitems = nsf * NB * nseg;
@@ -495,18 +472,17 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     const int tend = jb + D;
 
     const int trow = (int)((s * 4 + fi) * N + (long long)b * H);
-    // buffer of tile jt: (jt - jst) & 1 (IIR, two buffers), else 0
-    auto land = [&](int jt, int bi) {
+    auto land = [&](int jt) {
       if (tid == 0 && !(dbgm & 8)) {
         fence_proxy_async();
-        const unsigned bar = smem_u32(oBar + 2 * bi);
+        const unsigned bar = smem_u32(oBar);
         mbar_expect_tx(bar, H * PF * 4);
-        tma_load_2d(smem_u32(bi * H * PF), &tmapF, jt * X - 8, trow, bar);
+        tma_load_2d(smem_u32(oF), &tmapF, jt * X - 8, trow, bar);
       }
     };
-    auto tma_wait = [&](int bi) {
-      if (!(dbgm & 8)) mbar_wait(smem_u32(oBar + 2 * bi), (ph >> bi) & 1u);
-      ph ^= 1u << bi;
+    auto tma_wait = [&]() {
+      if (!(dbgm & 8)) mbar_wait(smem_u32(oBar), ph & 1);
+      ph ^= 1u;
     };
     // L2 prefetch of raw tile jt (TMA, no shared memory): the landing of a tile is
     // issued one step ahead, its first touch of HBM PF tiles ahead
@@ -514,9 +490,8 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     auto prefetch = [&](int jt) {
       if (tid == 0 && jt < nt && !(dbgm & 8)) tma_prefetch_2d(&tmapF, jt * X - 8, trow);
     };
-    land(jst, 0);
-    if (NFB == 2 && jst + 1 < nt && jst + 1 < tend) land(jst + 1, 1);
-    for (int i = NFB; i < NFB + PFD; ++i) prefetch(jst + i);
+    land(jst);
+    for (int i = 1; i <= PFD; ++i) prefetch(jst + i);
     // S1 halo of the first stored tile: zero (its outputs are never read, but keep
     // them finite)
     for (int e = tid; e < H * (HS / 4); e += NT) {
@@ -529,13 +504,11 @@ __global__ void __launch_bounds__(H * X / 32, 3)
     for (int t = jst; t < tend; ++t, slot_t = (slot_t == D) ? 0 : slot_t + 1) {
       const int j = t - D;
       const bool back = j >= j1;
-      const int bi = (NFB == 2) ? ((t - jst) & 1) : 0;   // tile buffer of this iteration
-      const int fb = bi * H * PF;
       if (IIR) {
-        if (t < nt) tma_wait(bi);                        // raw tile t landed
+        if (t < nt) tma_wait();                          // raw tile t landed
         if (t < nt && !(dbgm & 32)) {
           // ---- front: zero-state sweeps of this thread's chunk ----
-          const int rowF = fb + ir * PF + HF + 32 * iq;
+          const int rowF = oF + ir * PF + HF + 32 * iq;
           float x[32];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -718,7 +691,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           float P[32];
           tmem_wait_st();
           tmem_ld32(tbase + 32u * slot_j, P);
-          const int rowF = fb + ir * PF + HF + 32 * iq;
+          const int rowF = oF + ir * PF + HF + 32 * iq;
           // homogeneous anticausal response at sample i: sum_m (A^(32-i))_{0m} tm_m,
           // adjacent samples packed (plan table k.GA)
           const float2 t0 = make_float2(tm[0], tm[0]), t1 = make_float2(tm[1], tm[1]),
@@ -737,13 +710,13 @@ __global__ void __launch_bounds__(H * X / 32, 3)
           }
         }
       } else {
-        tma_wait(0);                                     // raw tile j = F(j) landed
+        tma_wait();                                      // raw tile j = F(j) landed
       }
       if (back && iq < 2) {
         // halo: F(j-1)'s last HF columns (zero at the first back tile), written by the
         // row's own chunk threads 0 and 1
         const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + ir * HF + 4 * iq);
-        st4(fb + ir * PF + 4 * iq, h);
+        st4(oF + ir * PF + 4 * iq, h);
       }
       // F(j) rows 8G .. 8G+7 are complete: they were written by the same threads that
       // run step 1 on them (row group G = the IIR threads of rows 8G..8G+7)
@@ -754,7 +727,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
         static_assert(NCH == 8 * TPR, "step-1 row group = the IIR threads of its rows");
         const int jj = tid % NCH, G = Gt;
         float2 v[8][It<3, C1>::T / 2];
-        item_load<3, C1>(fb + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
+        item_load<3, C1>(oF + (G * 8) * PF + C1 * jj, PF, 0, v);   // HF + C1*jj - O(=8)
         item_fht<3, C1>(v);
         const int gb = G & (NR2 - 1);                   // next step's block index
         // outputs shifted by their step-2 pre-shift (r*gb) mod 4 (scalar stores: the
@@ -767,16 +740,14 @@ __global__ void __launch_bounds__(H * X / 32, 3)
         }
       }
       // stash this tile's last HF filtered columns (halo of the next tile), row owners
-      if (back && iq < 2) st4(oStash + ir * HF + 4 * iq, ld4(fb + ir * PF + X + 4 * iq));
+      if (back && iq < 2) st4(oStash + ir * HF + 4 * iq, ld4(oF + ir * PF + X + 4 * iq));
       __syncthreads();                                   // F read by all (landing); S1 complete (step 2)
       // F is free: land the next raw tile
       if (IIR) {
-        // this iteration's buffer is free (front, step 1 and the stash have read it):
-        // tile t + NFB lands into it
-        if (t + NFB < nt && t + NFB < tend) land(t + NFB, bi);
-        prefetch(t + NFB + PFD);
+        if (t + 1 < nt && t + 1 < tend) land(t + 1);
+        prefetch(t + 1 + PFD);
       } else if (j + 1 < jb) {
-        land(j + 1, 0);
+        land(j + 1);
         if (j + 1 + PFD < jb) prefetch(j + 1 + PFD);
       }
       if (back && j >= ja && !(dbgm & 2)) {
@@ -961,9 +932,6 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
   const int nsl = (int)(nitems / ((long long)nx * H));
   const PbPos step = pb_pos(gridDim.x, nx, H);
   const PbPos stepP = pb_pos((long long)g.P * gridDim.x, nx, H);
-#if FBP_KB_EF
-  const unsigned long long pol_ef = policy_evict_first();   // R is read once
-#endif
   auto issue = [&](const PbPos& pt, int bb) {
     if (tid != 0 || pt.sl >= nsl || (dbgm & 4)) return;
     if (g.P > 0) {
@@ -985,13 +953,8 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int xs = (q == 0) ? x02 : (N - x02 - XB);
-#if FBP_KB_EF
-      tma_load_3d_hint(smem_u32(oIn0 + bb * IN_SZ + q * NB * PI), &tmapR, xs - HI + NB, 0,
-                       (sl2 * 4 + 2 * PAIR + q) * H + ch2, bar, pol_ef);
-#else
       tma_load_3d(smem_u32(oIn0 + bb * IN_SZ + q * NB * PI), &tmapR, xs - HI + NB, 0,
                   (sl2 * 4 + 2 * PAIR + q) * H + ch2, bar);
-#endif
     }
   };
   PbPos cur = pb_pos(blockIdx.x, nx, H);
@@ -1180,13 +1143,12 @@ __global__ void __launch_bounds__(256, DB ? 3 : 2)
 // ---------------------------------------------------------------- host side
 bool sweep_supported(int N) { return N == 512 || N == 1024 || N == 2048 || N == 4096; }
 
-size_t sweep_a_smem(const SweepGeom& g, bool iir) {
+size_t sweep_a_smem(const SweepGeom& g) {
   const int H = g.H, X = g.X;
   const int R2 = (H == 64) ? 3 : 2;
   const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : 4 + 4 * ((7 * 3) / 4);
   const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
-  const int nfb = (iir && FBP_KS_DBUF) ? 2 : 1;
-  const size_t fl = (size_t)nfb * H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 8;
+  const size_t fl = (size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 8;
   return fl * sizeof(float);
 }
 
@@ -1245,7 +1207,7 @@ static cudaError_t launch_a_t(const float* lin, float* R, int slices, int f0, in
                               long long stride, const SweepGeom& g, const SweepIir& k, int* counter,
                               cudaStream_t st) {
   auto kern = k_sweep_a<H, X, IIR, BETA>;
-  size_t smem = sweep_a_smem(g, IIR);
+  size_t smem = sweep_a_smem(g);
   // tensor memory: (D+1) slots of 32 columns per lane; never more CTAs per SM than
   // the 512 columns hold (a CTA waiting in tcgen05.alloc would spin): raise the
   // shared-memory request so that the occupancy limit enforces it
