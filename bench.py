@@ -544,7 +544,7 @@ def run_fbp(args):
                               "unit": "GB/s per GPU",
                               # SURVEY 8(d)'s other figure: ncu DRAM bytes of all kernels of
                               # one call (committed bench-batch capture) over the live step time
-                              "ncu_dram": path_dram(B, ms_clean, world, peak)},
+                              "ncu_dram": path_dram(B, ms_clean / args.steps, world, peak)},
             "kernel_share": shares,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
             "gpu_launches": launches[0],

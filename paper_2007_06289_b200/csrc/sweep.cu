@@ -288,7 +288,7 @@ __device__ __forceinline__ void chunk_sweep(const float (&x)[32], float xl0, flo
 //   F      : H x PF  landing target of raw tile t (TMA box, columns tX-8 ..
 //            tX+X+4) and, once the IIR has read it, the filtered tile F(t-D):
 //            halo [0, HF) = F(t-D-1)'s last HF columns, core [HF, HF+X)
-//   stash  : H x HF  the core's last HF columns (halo of the next F tile)
+//   (stash : the core's last HF columns, the halo of the next F tile, in registers)
 //   S1     : H x PS  step-1 output, core [HS, HS+X), halo [0, HS)
 //   ring   : (D+1) x H x 3  anticausal tile aggregates agg[t]
 // Tensor memory (IIR): (D+1) slots x 32 columns per thread (its own lane): the
@@ -397,7 +397,10 @@ __global__ void __launch_bounds__(H * X / 32, 3)
   constexpr int HS = O2 + 4 * ((7 * (NR2 - 1)) / 4);   // step-2 input halo
   constexpr int PF = pitch4(HF + X + 4);
   constexpr int PS = pitch4(HS + X + 4);
-  constexpr int oF = 0, oStash = H * PF, oS = oStash + H * HF, oRing = oS + H * PS;
+  // F's last HF columns (the next tile's halo) stay in registers: chunk threads 0, 1
+  // of a row keep one quad each (r02 s5: 2 KB less shared memory per CTA puts three
+  // CTAs in the 164 KB carveout, doubling L1: KS 0.867 -> 0.839 ms)
+  constexpr int oF = 0, oS = H * PF, oRing = oS + H * PS;
   static_assert(X >= HS + 4, "S1 halo copy must not overlap its source");
   static_assert(NT == 128, "TMEM lanes: one per thread");
 
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       st4(oS + r * PS + 4 * qd, make_float4(0.f, 0.f, 0.f, 0.f));
     }
     float cin0 = 0.f, cin1 = 0.f, cin2 = 0.f;           // causal carry of the row
+    float4 stash = make_float4(0.f, 0.f, 0.f, 0.f);     // F(j)'s last HF columns, this thread's quad
     int slot_t = 0;                                      // ring / TMEM slot of tile t: (t - jst) mod (D+1)
 
     for (int t = jst; t < tend; ++t, slot_t = (slot_t == D) ? 0 : slot_t + 1) {
@@ -715,7 +719,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
       if (back && iq < 2) {
         // halo: F(j-1)'s last HF columns (zero at the first back tile), written by the
         // row's own chunk threads 0 and 1
-        const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(oStash + ir * HF + 4 * iq);
+        const float4 h = (j == j1) ? make_float4(0.f, 0.f, 0.f, 0.f) : stash;
         st4(oF + ir * PF + 4 * iq, h);
       }
       // F(j) rows 8G .. 8G+7 are complete: they were written by the same threads that
@@ -740,7 +744,7 @@ __global__ void __launch_bounds__(H * X / 32, 3)
         }
       }
       // stash this tile's last HF filtered columns (halo of the next tile), row owners
-      if (back && iq < 2) st4(oStash + ir * HF + 4 * iq, ld4(oF + ir * PF + X + 4 * iq));
+      if (back && iq < 2) stash = ld4(oF + ir * PF + X + 4 * iq);
       __syncthreads();                                   // F read by all (landing); S1 complete (step 2)
       // F is free: land the next raw tile
       if (IIR) {
@@ -1148,7 +1152,7 @@ size_t sweep_a_smem(const SweepGeom& g) {
   const int R2 = (H == 64) ? 3 : 2;
   const int HS = (R2 == 3) ? 8 + 4 * ((7 * 7) / 4) : 4 + 4 * ((7 * 3) / 4);
   const int PF = pitch4(8 + X + 4), PS = pitch4(HS + X + 4);
-  const size_t fl = (size_t)H * PF + (size_t)H * 8 + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 8;
+  const size_t fl = (size_t)H * PF + (size_t)H * PS + (size_t)(g.D + 1) * H * 3 + 4 + 8;
   return fl * sizeof(float);
 }
 
