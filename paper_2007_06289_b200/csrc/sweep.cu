@@ -382,7 +382,10 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 template <int H, int X, bool IIR, bool BETA>
-__global__ void __launch_bounds__(H * X / 32, 3)
+#ifndef FBP_KS_MINB
+#define FBP_KS_MINB 3
+#endif
+__global__ void __launch_bounds__(H * X / 32, FBP_KS_MINB)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k, int slices, int f0,
               int nf, long long lin_slice_stride, int nseg, int* __restrict__ counter,
               const __grid_constant__ CUtensorMap tmapF) {
