@@ -1356,6 +1356,9 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
   FBP_PAIR_CASE(32, 3, 2, 128)
   FBP_PAIR_CASE(32, 3, 2, 64)
   FBP_PAIR_CASE(64, 3, 3, 32)
+#if FBP_DEV_MASK
+  FBP_PAIR_CASE(64, 3, 3, 64)   // developer A/B only (FBP_XB=64): 133 KB per CTA, 1 CTA/SM
+#endif
 #undef FBP_PAIR_CASE
   if (launches) ++*launches;
   return e;
