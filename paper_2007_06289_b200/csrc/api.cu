@@ -377,9 +377,10 @@ fbp_status fbp_plan_create(fbp_plan** out, int n, int max_batch, int m, const do
 #if FBP_DEV_MASK
     if (const char* ev = std::getenv("FBP_PREFETCH")) sg.P = std::atoi(ev);
 #endif
-    // pass-B x-tile: 64 for NB = 32 (double-buffered TMA fills fit 2 CTAs/SM; measured
-    // 5 % faster than 128 single-buffered), 128 otherwise
-    sg.XB = (sg.NB == 64) ? 32 : (sg.NB == 32) ? 64 : 128;   // NB = 64 (N = 4096): radix 8+8, single-buffered
+    // pass-B x-tile: 64 for NB = 16 and 32 (double-buffered TMA fills at 3 CTAs/SM; measured
+    // 5 % faster than 128 single-buffered at NB = 32 and 31 % faster at NB = 16, N = 512),
+    // 32 for NB = 64 (N = 4096: radix 8+8, single-buffered; 64 measured 14 % slower)
+    sg.XB = (sg.NB == 64) ? 32 : 64;
 #if FBP_DEV_MASK
     // developer tuning knobs: compiled in only with -DFBP_DEV_MASK=1
     if (const char* ev = std::getenv("FBP_XB")) sg.XB = std::atoi(ev);

@@ -1352,7 +1352,10 @@ cudaError_t launch_pair_b(const float* R, float* img, int slices, int pair, floa
   if (g.NB == NBV && g.XB == XBV)                                                           \
     e = pair == 0 ? launch_b_t<R1, R2, XBV, 0>(R, img, slices, scale, g, st)                \
                   : launch_b_t<R1, R2, XBV, 1>(R, img, slices, scale, g, st);
-  FBP_PAIR_CASE(16, 2, 2, 128)
+  FBP_PAIR_CASE(16, 2, 2, 64)    // N = 512: double-buffered, 3 CTAs/SM (r02 s6: KB 0.619 -> 0.425 ms per 256 slices)
+#if FBP_DEV_MASK
+  FBP_PAIR_CASE(16, 2, 2, 128)   // developer A/B only (FBP_XB=128): the single-buffered r01 tile
+#endif
   FBP_PAIR_CASE(32, 3, 2, 128)
   FBP_PAIR_CASE(32, 3, 2, 64)
   FBP_PAIR_CASE(64, 3, 3, 32)
