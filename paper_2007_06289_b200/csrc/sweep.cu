@@ -382,8 +382,11 @@ __device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 template <int H, int X, bool IIR, bool BETA>
+// resident CTAs per SM the register budget is sized for: 4 for the H = 32 sweep (N = 512,
+// 1024: 128 registers without spills; r02 s6 A/B: KS -12 % / -8 %), 3 for H = 64
+// (N = 2048, 4096: 4 measured 25 % slower, 64 B of spills and no L1 left)
 #ifndef FBP_KS_MINB
-#define FBP_KS_MINB 3
+#define FBP_KS_MINB (H == 32 ? 4 : 3)
 #endif
 __global__ void __launch_bounds__(H * X / 32, FBP_KS_MINB)
     k_sweep_a(const float* __restrict__ lin, float* __restrict__ Rout, SweepGeom g, SweepIir k, int slices, int f0,
